@@ -1,0 +1,227 @@
+/*
+ * ed_batch.h — C ABI of the B200-native ED-Batch hot path (libedbatch.so).
+ *
+ * What it computes (arXiv 2302.03851, PAPER.md):
+ *   ed_plan     Alg. 1 "FSM-based Dynamic Batching" over the disjoint union of
+ *               per-instance dataflow graphs, with the E_sort state encoding and a
+ *               given FSM transition table pi(S); then a memory layout of the
+ *               node outputs (§3: results and sources of each batch contiguous and
+ *               aligned where possible); then lowering to a device step table.
+ *   ed_execute  runs the whole batch schedule as ONE persistent sm_100a kernel: per batch,
+ *               gather (or block-read) operand rows, the cell's dense contraction (tcgen05/TMEM
+ *               for bf16, FFMA for fp32), fused gate epilogue, contiguous result store; grid-wide
+ *               barrier between batches (removing the per-batch launch overhead of P:40).
+ *
+ * Conventions for every call:
+ *   - Return value: ED_OK (0) or a negative ed_status_t; on failure a thread-local message is
+ *     available from ed_last_error() until the next failing call on the same thread.
+ *   - Host arrays passed in are BORROWED for the duration of the call only.
+ *   - Device pointers are caller-owned (PyTorch tensors); the library never allocates device
+ *     memory (no cudaMalloc) and never synchronises the host with the device inside ed_execute.
+ *   - Streams are cudaStream_t passed as void* (0 = legacy default stream).
+ */
+#ifndef ED_BATCH_H
+#define ED_BATCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ed_status_t;
+
+#define ED_OK               0
+#define ED_E_INVALID_ARG   -1  /* null pointer, bad size, bad CSR offsets, bad ext id        */
+#define ED_E_CYCLE         -2  /* an instance graph is not acyclic (Alg. 1 needs a DAG)       */
+#define ED_E_DANGLING      -3  /* node input / root refers to a node id outside the instance  */
+#define ED_E_DUP_ID        -4  /* reserved: CSR ids are implicit, so duplicates cannot occur  */
+#define ED_E_TYPE          -5  /* op type index out of range or unsupported cell/dtype mix    */
+#define ED_E_ARITY         -6  /* number of inputs does not match the op type's slots         */
+#define ED_E_FSM           -7  /* malformed FSM table (bad key, action not in its key)        */
+#define ED_E_CUDA          -8  /* a CUDA runtime call failed                                  */
+#define ED_E_UNSUPPORTED   -9  /* device is not sm_100 or the plan needs an unbuilt variant   */
+#define ED_E_WORKSPACE    -10  /* workspace pointer null/misaligned or smaller than required  */
+#define ED_E_OOM          -11  /* host allocation failed                                      */
+
+/* Slot value meaning "zero state" (h_{-1} = c_{-1} = 0), read from a dedicated zero row. */
+#define ED_ZERO_INPUT INT32_MIN
+
+/* Cell kinds (equations: DESIGN.md §3 / SURVEY App. A; the paper only cites them). */
+#define ED_CELL_TREELSTM_LEAF      1  /* Table 4 P:364.  x = emb[ext]; [i;o;u] = W x + b          */
+#define ED_CELL_TREELSTM_INTERNAL  2  /* Table 4 P:363.  slots (l, r); [i;f_l;f_r;o;u] = U[h_l;h_r] */
+#define ED_CELL_LINEAR_OUT         3  /* output op O (Fig. 1): y = W h + b, fp32 logits     */
+#define ED_CELL_TREEGRU_LEAF       4  /* Table 4                                            */
+#define ED_CELL_TREEGRU_INTERNAL   5  /* Table 4                                            */
+#define ED_CELL_TREEFC_INTERNAL    6  /* h = tanh(W[h_l;h_r] + b); slots may be external words   */
+#define ED_CELL_LSTM               7  /* BiLSTM F/B cell: x = emb[ext], slot = h_prev     */
+#define ED_CELL_TAGGER             8  /* y = W2 tanh(W1[h_f;h_b] + b1) + b2                       */
+#define ED_CELL_MVRNN_INTERNAL     9  /* MV-RNN (Table 4)                            */
+#define ED_CELL_LATTICE_CHAR      10  /* LatticeLSTM char cell (Fig. 7), variadic    */
+#define ED_CELL_LATTICE_WORD      11  /* LatticeLSTM word cell                                     */
+
+#define ED_FP32 0
+#define ED_BF16 1
+
+#define ED_ENC_SORT 0   /* E_sort: frontier types by descending count, ties ascending id */
+#define ED_ENC_BASE 1   /* E_base: ascending set of frontier types                                 */
+
+#define ED_FALLBACK_KEY0 0  /* table miss or action not ready: take key[0] (reading A-3) */
+
+#define ED_LAYOUT_SCHEDULE_ORDER 0  /* rows in schedule order: results contiguous, sources gathered */
+#define ED_LAYOUT_PQ             1  /* PQ-tree plan (§3.2, Alg. 2-6) over the node-output rows      */
+
+/* One op type ("each operation is given a type"). */
+typedef struct {
+  int32_t cell_kind;   /* ED_CELL_*                                                         */
+  int32_t num_slots;   /* fixed input slots (variadic cells: the fixed prefix)              */
+  int32_t variadic;    /* 1: node inputs after the fixed slots are a variable-length list   */
+  int32_t has_ext;     /* 1: the op reads emb[ext[v]] of its weight set                     */
+  int32_t weight_set;  /* index into ed_weights_t.sets                                      */
+  int32_t hidden;      /* h; every type of one plan must share it                          */
+  int32_t out_dim;     /* logits width for ED_CELL_LINEAR_OUT / ED_CELL_TAGGER, else 0      */
+  int32_t dtype;       /* ED_BF16 | ED_FP32; every type of one plan must share it          */
+} ed_op_type_t;
+
+/* One instance graph in CSR form (node ids are 0..num_nodes-1, implicit).
+ *   type[v]          op type index
+ *   in_off[v..v+1]   range of in_idx holding v's inputs in slot order (in_off[0] == 0)
+ *   in_idx[k] >= 0   local node id;  == ED_ZERO_INPUT: zero state;  other < 0: external
+ *                    input id (-1 - id) read from the type's embedding table (word leaves)
+ *   ext[v]           token id for has_ext types, else ignored (may be NULL if no type has ext)
+ *   root             local node id whose h is the instance output, or (-1 - id) for an
+ *                    instance with no ops whose output is the external row itself          */
+typedef struct {
+  int32_t num_nodes;
+  const int32_t *type;
+  const int32_t *in_off;
+  const int32_t *in_idx;
+  const int32_t *ext;
+  int32_t root;
+} ed_graph_t;
+
+/* FSM transition table pi (Fig. 2; P:140 constant-time lookup): key = E(G) as a
+ * list of type ids, action = the type to batch next. */
+typedef struct {
+  int32_t key_len;
+  const int32_t *key;
+  int32_t action;
+} ed_fsm_entry_t;
+
+typedef struct {
+  int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE */
+  int32_t num_entries;
+  const ed_fsm_entry_t *entries;
+  int32_t fallback;      /* ED_FALLBACK_KEY0 */
+} ed_fsm_t;
+
+typedef struct {
+  int32_t layout;        /* ED_LAYOUT_SCHEDULE_ORDER | ED_LAYOUT_PQ */
+  int32_t reserved[7];   /* must be 0 */
+} ed_plan_opts_t;
+
+typedef struct ed_plan_s ed_plan_t;  /* opaque plan handle */
+
+typedef struct {
+  int64_t num_nodes;          /* V (all instances)                                        */
+  int64_t num_instances;
+  int64_t num_batches;        /* length of the schedule                                   */
+  int64_t lower_bound;        /* sum_t Depth(G_t) (App. B.3)                   */
+  int64_t num_rows;           /* V + 1 (row V is the all-zero row)                        */
+  int64_t hidden;
+  int64_t dtype;
+  int64_t workspace_bytes;    /* minimum size of the ed_execute workspace                 */
+  int64_t contig_operands;    /* (batch, fixed slot) operands read as one block           */
+  int64_t gather_operands;    /* (batch, fixed slot) operands read by row index           */
+  int64_t copy_bytes;         /* gather+scatter bytes a copy-based executor would move    */
+  int64_t copy_kernels;       /* gather+scatter kernels a copy-based executor would launch */
+  int64_t off_h;              /* workspace byte offsets of the row buffers:               */
+  int64_t off_c;              /*   H [num_rows x hidden] (dtype), C [num_rows x hidden] f32 */
+  int64_t off_y;              /*   Y [num_rows x y_cols] f32 (logits of output ops)       */
+  int64_t y_cols;
+  int64_t off_x;              /*   X [num_rows x hidden] f32 (lattice link gates)         */
+  int64_t off_ts;             /*   u64 %globaltimer stamp after each batch (num_batches+1) */
+  double plan_us;             /* host time spent in ed_plan                               */
+  double schedule_us;
+  double layout_us;
+} ed_plan_info_t;
+
+/* Per weight set, device pointers.  Matrices must have been packed by ed_pack_weights.
+ *   W     packed main matrix of the cell (logical [G*h, K] rows = gate-stacked outputs)
+ *   b     fp32 bias [G*h] (logical order)
+ *   W2,b2 second matrix (TAGGER: [C, h]; LATTICE_WORD: link gate [h, 2h]; MVRNN: W_M [h, 2h])
+ *   emb   embedding table [emb_rows, h] (dtype of the plan); emb2 second table (lattice chars)
+ *   mat   MV-RNN word matrices [emb_rows, h, h] (dtype of the plan)                        */
+typedef struct {
+  const void *W;
+  const float *b;
+  const void *W2;
+  const float *b2;
+  const void *emb;
+  const void *emb2;
+  const void *mat;
+  int32_t emb_rows;
+  int32_t emb2_rows;
+} ed_weight_set_t;
+
+typedef struct {
+  int32_t num_sets;
+  const ed_weight_set_t *sets;
+} ed_weights_t;
+
+typedef struct {
+  void *out_root;   /* [num_instances x hidden] in the plan dtype: root h of each instance, in
+                       instance order (may be NULL) */
+  uint64_t *trace;  /* optional device buffer [num_batches x 8] of %globaltimer stamps taken by
+                       CTA 0 at fixed phases of each batch (profiling aid; NULL = off) */
+} ed_io_t;
+
+/* Build a plan (host only; no CUDA call).  Validates the graphs (errors above), merges them
+ * (instance-major global ids), runs Alg. 1 with the table, plans the layout, lowers it. */
+ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_type_t *types,
+                    int32_t num_types, const ed_fsm_t *fsm, const ed_plan_opts_t *opts,
+                    ed_plan_t **out);
+
+ed_status_t ed_plan_info(const ed_plan_t *plan, ed_plan_info_t *out);
+
+/* Schedule of the plan (Alg. 1 output): batch_type[num_batches], batch_off[num_batches+1],
+ * members[num_nodes] = global node ids, each batch in position (= ascending row) order. */
+ed_status_t ed_plan_get_schedule(const ed_plan_t *plan, int32_t *batch_type, int32_t *batch_off,
+                                 int32_t *members);
+
+/* row_of_node[num_nodes]: row of each global node's output record in the H/C/Y buffers. */
+ed_status_t ed_plan_get_layout(const ed_plan_t *plan, int32_t *row_of_node);
+
+/* Per (batch, fixed slot) flag: 1 = contiguous block read, 0 = gathered. [num_batches * 2] */
+ed_status_t ed_plan_get_slot_modes(const ed_plan_t *plan, int32_t *modes);
+
+void ed_plan_destroy(ed_plan_t *plan);
+
+/* Bytes of the packed form of a logical matrix.  which = 0: main W; 1: W2. */
+int64_t ed_packed_bytes(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which);
+
+/* Pack a logical fp32 matrix (device, row-major [rows, cols] as in DESIGN.md §5) into the
+ * device layout the kernels read: bf16 gate-interleaved, K-major, 128B-swizzled UMMA canonical
+ * tiles; fp32 transposed for FFMA.  Asynchronous on stream. */
+ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which,
+                            const float *logical_dev, void *packed_dev, void *stream);
+
+/* Execute the plan: one persistent cooperative kernel on `stream`.  The first execute on a
+ * given workspace also uploads the step table (async H2D) and zeroes the zero row.  Results:
+ * node records in the workspace row buffers (offsets in ed_plan_info_t) and io->out_root. */
+ed_status_t ed_execute(ed_plan_t *plan, const ed_weights_t *weights, const ed_io_t *io, void *workspace,
+                       size_t workspace_bytes, void *stream);
+
+/* Number of kernels ed_execute launches (for launch accounting). */
+int32_t ed_execute_launch_count(const ed_plan_t *plan);
+
+/* Version string and build arch, e.g. "ed_batch 0.1 sm_100a". */
+const char *ed_version(void);
+
+const char *ed_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ED_BATCH_H */

@@ -1,0 +1,608 @@
+// ed_batch.cpp — host side of libedbatch.so: C ABI (include/ed_batch.h), graph ingest and
+// validation, Alg. 1 FSM frontier scheduler, layout planning, lowering to the device step table.
+//
+// PAPER.md references: Alg. 1; types; E_sort; policy lookup;
+// lower bound (App. B.3); memory layout (§3).  Readings: DESIGN.md §3.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include <cuda_runtime.h>
+
+#include "ed_batch.h"
+#include "ed_internal.h"
+#include "ed_layout.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows x cols] tensor map with 128B swizzle, box {64, box_rows}.
+bool encode_rows(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || !base || rows <= 0) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {64, box_rows}, es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+ed_status_t fail(ed_status_t code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct ed_plan_s {
+  // types
+  std::vector<ed_op_type_t> types;
+  int hidden = 0, dtype = 0;
+  // merged graph (global ids)
+  int64_t V = 0;
+  int32_t ninst = 0;
+  std::vector<int32_t> gtype, in_off, in_idx, ext;  // in_idx: >=0 global node, ZERO, or -1-id external
+  std::vector<int32_t> roots;                         // global node id or -1-id
+  // schedule
+  std::vector<int32_t> batch_type, batch_off, members;
+  int64_t lower_bound = 0;
+  // layout
+  std::vector<int32_t> row_of_node;
+  std::vector<int32_t> slot_modes;
+  // lowering
+  std::vector<ed::DevStep> steps;
+  std::vector<int32_t> idx;
+  std::vector<int32_t> root_rows;
+  int root_wset = 0;
+  // workspace layout
+  size_t off_bar = 0, off_ts = 0, off_steps = 0, off_idx = 0, off_roots = 0, off_h = 0, off_c = 0, off_y = 0,
+         off_x = 0, ws_bytes = 0;
+  int64_t y_cols = 0;
+  bool need_x = false;
+  // stats
+  int64_t contig = 0, gather = 0, copy_bytes = 0, copy_kernels = 0;
+  double plan_us = 0, sched_us = 0, layout_us = 0;
+  // upload state
+  std::vector<uint8_t> blob;          // [ts zeros | steps | idx | roots]
+  void *pinned = nullptr;
+  const void *uploaded_ws = nullptr;
+  int grid = 0;
+  uint32_t launches = 0;
+};
+
+// ------------------------------------------------------------------------------------------------
+// validation + merge (SURVEY A-5, A-24)
+// ------------------------------------------------------------------------------------------------
+static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, int32_t ng) {
+  const int nt = static_cast<int>(pl->types.size());
+  int64_t total = 0;
+  for (int gi = 0; gi < ng; ++gi) {
+    const ed_graph_t &g = graphs[gi];
+    if (g.num_nodes < 0) return fail(ED_E_INVALID_ARG, "graph " + std::to_string(gi) + ": negative num_nodes");
+    if (g.num_nodes > 0 && (!g.type || !g.in_off))
+      return fail(ED_E_INVALID_ARG, "graph " + std::to_string(gi) + ": null type/in_off");
+    total += g.num_nodes;
+  }
+  if (total >= (int64_t(1) << 30)) return fail(ED_E_INVALID_ARG, "too many nodes");
+  pl->V = total;
+  pl->ninst = ng;
+  pl->gtype.resize(total);
+  pl->in_off.assign(total + 1, 0);
+  pl->ext.assign(total, -1);
+  pl->roots.resize(ng);
+  int64_t base = 0;
+  for (int gi = 0; gi < ng; ++gi) {
+    const ed_graph_t &g = graphs[gi];
+    const std::string tag = "graph " + std::to_string(gi);
+    const int n = g.num_nodes;
+    if (n > 0 && g.in_off[0] != 0) return fail(ED_E_INVALID_ARG, tag + ": in_off[0] != 0");
+    for (int v = 0; v < n; ++v) {
+      if (g.in_off[v + 1] < g.in_off[v]) return fail(ED_E_INVALID_ARG, tag + ": in_off not monotone");
+      const int t = g.type[v];
+      if (t < 0 || t >= nt) return fail(ED_E_TYPE, tag + ": node " + std::to_string(v) + " has unknown type");
+      const ed_op_type_t &ot = pl->types[t];
+      const int deg = g.in_off[v + 1] - g.in_off[v];
+      if (ot.variadic ? deg < ot.num_slots : deg != ot.num_slots)
+        return fail(ED_E_ARITY, tag + ": node " + std::to_string(v) + " has " + std::to_string(deg) +
+                                    " inputs, type expects " + std::to_string(ot.num_slots));
+      if (deg > 0 && !g.in_idx) return fail(ED_E_INVALID_ARG, tag + ": null in_idx");
+      for (int k = g.in_off[v]; k < g.in_off[v + 1]; ++k) {
+        const int x = g.in_idx[k];
+        if (x >= 0) {
+          if (x >= n) return fail(ED_E_DANGLING, tag + ": node " + std::to_string(v) + " input " + std::to_string(x) + " out of range");
+          if (x == v) return fail(ED_E_CYCLE, tag + ": self loop at node " + std::to_string(v));
+          pl->in_idx.push_back(static_cast<int32_t>(base + x));
+        } else {
+          pl->in_idx.push_back(x);  // ED_ZERO_INPUT or external (-1 - id)
+        }
+      }
+      pl->gtype[base + v] = t;
+      pl->in_off[base + v + 1] = static_cast<int32_t>(pl->in_idx.size());
+      if (ot.has_ext) {
+        if (!g.ext) return fail(ED_E_INVALID_ARG, tag + ": type with ext but ext == NULL");
+        if (g.ext[v] < 0) return fail(ED_E_INVALID_ARG, tag + ": node " + std::to_string(v) + " has no ext token");
+        pl->ext[base + v] = g.ext[v];
+      }
+    }
+    if (g.root >= n) return fail(ED_E_DANGLING, tag + ": root out of range");
+    if (g.root < 0 && n > 0) return fail(ED_E_DANGLING, tag + ": external root on a graph with ops");
+    pl->roots[gi] = g.root >= 0 ? static_cast<int32_t>(base + g.root) : g.root;
+    base += n;
+  }
+  // acyclicity (Kahn)
+  std::vector<int32_t> indeg(total, 0);
+  std::vector<int32_t> coff(total + 1, 0);
+  for (int64_t v = 0; v < total; ++v)
+    for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+      if (pl->in_idx[k] >= 0) { ++indeg[v]; ++coff[pl->in_idx[k] + 1]; }
+  for (int64_t v = 0; v < total; ++v) coff[v + 1] += coff[v];
+  std::vector<int32_t> cons(coff[total]);
+  {
+    std::vector<int32_t> fill(coff.begin(), coff.end() - 1);
+    for (int64_t v = 0; v < total; ++v)
+      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+        if (pl->in_idx[k] >= 0) cons[fill[pl->in_idx[k]]++] = static_cast<int32_t>(v);
+  }
+  std::vector<int32_t> stack;
+  for (int64_t v = 0; v < total; ++v)
+    if (indeg[v] == 0) stack.push_back(static_cast<int32_t>(v));
+  int64_t seen = 0;
+  std::vector<int32_t> d = indeg;
+  while (!stack.empty()) {
+    const int32_t v = stack.back();
+    stack.pop_back();
+    ++seen;
+    for (int k = coff[v]; k < coff[v + 1]; ++k)
+      if (--d[cons[k]] == 0) stack.push_back(cons[k]);
+  }
+  if (seen != total) return fail(ED_E_CYCLE, "dataflow graph has a cycle");
+  return ED_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Alg. 1 with E_sort / E_base + table lookup; fallback key[0] (A-3)
+// ------------------------------------------------------------------------------------------------
+static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
+  const int nt = static_cast<int>(pl->types.size());
+  const int64_t V = pl->V;
+  std::map<std::vector<int32_t>, int32_t> table;
+  int encoder = ED_ENC_SORT;
+  if (fsm) {
+    encoder = fsm->encoder;
+    if (encoder != ED_ENC_SORT && encoder != ED_ENC_BASE) return fail(ED_E_FSM, "unknown encoder");
+    if (fsm->fallback != ED_FALLBACK_KEY0) return fail(ED_E_FSM, "unknown fallback");
+    if (fsm->num_entries > 0 && !fsm->entries) return fail(ED_E_FSM, "null entries");
+    for (int e = 0; e < fsm->num_entries; ++e) {
+      const ed_fsm_entry_t &en = fsm->entries[e];
+      if (en.key_len <= 0 || en.key_len > nt || !en.key) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": bad key");
+      std::vector<int32_t> key(en.key, en.key + en.key_len);
+      std::vector<int32_t> sorted_key = key;
+      std::sort(sorted_key.begin(), sorted_key.end());
+      for (int k = 0; k < en.key_len; ++k) {
+        if (key[k] < 0 || key[k] >= nt) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": key type out of range");
+        if (k > 0 && sorted_key[k] == sorted_key[k - 1]) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": repeated type in key");
+      }
+      if (std::find(key.begin(), key.end(), en.action) == key.end())
+        return fail(ED_E_FSM, "entry " + std::to_string(e) + ": action not present in its key");
+      table[key] = en.action;
+    }
+  }
+  // consumers CSR and remaining-input counters (one count per node-input edge)
+  std::vector<int32_t> remaining(V, 0), coff(V + 1, 0);
+  for (int64_t v = 0; v < V; ++v)
+    for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+      if (pl->in_idx[k] >= 0) { ++remaining[v]; ++coff[pl->in_idx[k] + 1]; }
+  for (int64_t v = 0; v < V; ++v) coff[v + 1] += coff[v];
+  std::vector<int32_t> cons(coff[V]);
+  {
+    std::vector<int32_t> fill(coff.begin(), coff.end() - 1);
+    for (int64_t v = 0; v < V; ++v)
+      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+        if (pl->in_idx[k] >= 0) cons[fill[pl->in_idx[k]]++] = static_cast<int32_t>(v);
+  }
+  std::vector<std::vector<int32_t>> ready(nt);
+  for (int64_t v = 0; v < V; ++v)
+    if (remaining[v] == 0) ready[pl->gtype[v]].push_back(static_cast<int32_t>(v));
+  pl->batch_type.clear();
+  pl->batch_off.assign(1, 0);
+  pl->members.clear();
+  pl->members.reserve(V);
+  std::vector<int32_t> key, order(nt);
+  int64_t done = 0;
+  while (done < V) {
+    key.clear();
+    for (int t = 0; t < nt; ++t)
+      if (!ready[t].empty()) key.push_back(t);
+    if (key.empty()) return fail(ED_E_CYCLE, "no ready node (internal)");
+    std::vector<int32_t> skey = key;  // E_sort: descending count, ties ascending id
+    std::stable_sort(skey.begin(), skey.end(), [&](int a, int b) { return ready[a].size() > ready[b].size(); });
+    const std::vector<int32_t> &lookup = encoder == ED_ENC_SORT ? skey : key;
+    int32_t act = -1;
+    auto it = table.find(lookup);
+    if (it != table.end()) act = it->second;
+    if (act < 0 || ready[act].empty()) act = skey[0];
+    std::vector<int32_t> batch;
+    batch.swap(ready[act]);
+    std::sort(batch.begin(), batch.end());
+    for (int32_t v : batch) {
+      pl->members.push_back(v);
+      for (int k = coff[v]; k < coff[v + 1]; ++k) {
+        const int32_t w = cons[k];
+        if (--remaining[w] == 0) ready[pl->gtype[w]].push_back(w);
+      }
+    }
+    done += static_cast<int64_t>(batch.size());
+    pl->batch_type.push_back(act);
+    pl->batch_off.push_back(static_cast<int32_t>(pl->members.size()));
+  }
+  // App. B.3 lower bound: per type, the max number of type-t nodes on a path (= Depth(G^t)).
+  std::vector<int32_t> topo(pl->members);  // schedule order is a topological order
+  int64_t lb = 0;
+  std::vector<int32_t> cnt(V);
+  for (int t = 0; t < nt; ++t) {
+    int32_t best = 0;
+    for (int32_t v : topo) {
+      int32_t c = 0;
+      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+        if (pl->in_idx[k] >= 0) c = std::max(c, cnt[pl->in_idx[k]]);
+      cnt[v] = c + (pl->gtype[v] == t ? 1 : 0);
+      best = std::max(best, cnt[v]);
+    }
+    lb += best;
+  }
+  pl->lower_bound = lb;
+  return ED_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// lowering: node rows -> device step table
+// ------------------------------------------------------------------------------------------------
+static ed_status_t lower(ed_plan_t *pl) {
+  const int64_t V = pl->V;
+  const int zero_row = static_cast<int32_t>(V);
+  const int nb = static_cast<int>(pl->batch_type.size());
+  const int h = pl->hidden;
+  pl->steps.assign(nb, ed::DevStep{});
+  pl->idx.clear();
+  pl->slot_modes.assign(static_cast<size_t>(nb) * 2, -1);
+  pl->contig = pl->gather = pl->copy_bytes = pl->copy_kernels = 0;
+  const int64_t row_bytes = static_cast<int64_t>(h) * (pl->dtype == ED_BF16 ? 2 : 4);
+  auto encode = [&](int32_t x) -> int32_t {
+    if (x >= 0) return pl->row_of_node[x];
+    if (x == ED_ZERO_INPUT) return zero_row;
+    return x;  // external id
+  };
+  for (int b = 0; b < nb; ++b) {
+    const int t = pl->batch_type[b];
+    const ed_op_type_t &ot = pl->types[t];
+    std::vector<int32_t> mem(pl->members.begin() + pl->batch_off[b], pl->members.begin() + pl->batch_off[b + 1]);
+    std::sort(mem.begin(), mem.end(), [&](int32_t a, int32_t c) { return pl->row_of_node[a] < pl->row_of_node[c]; });
+    std::copy(mem.begin(), mem.end(), pl->members.begin() + pl->batch_off[b]);
+    const int m = static_cast<int>(mem.size());
+    ed::DevStep &st = pl->steps[b];
+    st.cell = ot.cell_kind;
+    st.m = m;
+    st.out_row0 = pl->row_of_node[mem[0]];
+    for (int i = 0; i < m; ++i)
+      if (pl->row_of_node[mem[i]] != st.out_row0 + i)
+        return fail(ED_E_INVALID_ARG, "internal: result operand of batch " + std::to_string(b) + " not contiguous");
+    st.wset = ot.weight_set;
+    st.ext_off = -1;
+    st.var_off = -1;
+    st.gates = ed::cell_gates(ot.cell_kind);
+    st.units = ed::cell_units(ot.cell_kind);
+    st.n_col_tiles = st.units > 0 ? h / st.units : 0;
+    st.nslots = std::min(ot.num_slots, ed::kMaxSlotsDev);
+    for (int j = 0; j < st.nslots; ++j) {
+      std::vector<int32_t> ent(m);
+      bool contig = true;
+      for (int i = 0; i < m; ++i) {
+        ent[i] = encode(pl->in_idx[pl->in_off[mem[i]] + j]);
+        const int32_t raw = pl->in_idx[pl->in_off[mem[i]] + j];
+        if (raw < 0 || ent[i] != ent[0] + i) contig = false;
+      }
+      if (contig) {
+        st.mode[j] = 1;
+        st.arg[j] = ent[0];
+        ++pl->contig;
+      } else {
+        st.mode[j] = 0;
+        st.arg[j] = static_cast<int32_t>(pl->idx.size());
+        pl->idx.insert(pl->idx.end(), ent.begin(), ent.end());
+        ++pl->gather;
+        pl->copy_bytes += 2 * static_cast<int64_t>(m) * row_bytes;
+        ++pl->copy_kernels;
+      }
+      pl->slot_modes[static_cast<size_t>(b) * 2 + j] = st.mode[j];
+    }
+    if (ot.has_ext) {
+      st.ext_off = static_cast<int32_t>(pl->idx.size());
+      for (int i = 0; i < m; ++i) pl->idx.push_back(pl->ext[mem[i]]);
+    }
+    if (ot.variadic) {
+      st.var_off = static_cast<int32_t>(pl->idx.size());
+      const size_t offs = pl->idx.size();
+      pl->idx.resize(offs + m + 1);
+      for (int i = 0; i < m; ++i) {
+        pl->idx[offs + i] = static_cast<int32_t>(pl->idx.size());
+        for (int k = pl->in_off[mem[i]] + ot.num_slots; k < pl->in_off[mem[i] + 1]; ++k)
+          pl->idx.push_back(encode(pl->in_idx[k]));
+      }
+      pl->idx[offs + m] = static_cast<int32_t>(pl->idx.size());
+    }
+  }
+  pl->root_rows.resize(pl->ninst);
+  for (int i = 0; i < pl->ninst; ++i) {
+    const int32_t r = pl->roots[i];
+    pl->root_rows[i] = r >= 0 ? pl->row_of_node[r] : r;
+  }
+  // workspace layout
+  const int64_t rows = V + 1;
+  const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
+  size_t off = 0;
+  pl->off_bar = off; off += 256 + 256 * 1024;  // counter + per-CTA flags (256 B apart)
+  pl->off_ts = off; off = align_up(off + 8 * static_cast<size_t>(nb + 1), 256);
+  pl->off_steps = off; off = align_up(off + sizeof(ed::DevStep) * nb, 256);
+  pl->off_idx = off; off = align_up(off + 4 * pl->idx.size(), 256);
+  pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 256);
+  pl->off_h = off; off = align_up(off + elt * rows * h, 1024);
+  pl->off_c = off; off = align_up(off + 4 * rows * h, 1024);
+  pl->y_cols = 0;
+  pl->need_x = false;
+  for (const auto &ot : pl->types) {
+    if (ot.cell_kind == ED_CELL_LINEAR_OUT || ot.cell_kind == ED_CELL_TAGGER)
+      pl->y_cols = std::max<int64_t>(pl->y_cols, ot.out_dim);
+    if (ot.cell_kind == ED_CELL_LATTICE_WORD) pl->need_x = true;
+  }
+  pl->off_y = off; off = align_up(off + 4 * rows * pl->y_cols, 1024);
+  pl->off_x = off; if (pl->need_x) off = align_up(off + 4 * rows * h, 1024);
+  pl->ws_bytes = off;
+  // host blob mirrors [ts .. roots] so one async H2D uploads the static part
+  pl->blob.assign(pl->off_h - pl->off_ts, 0);
+  std::memcpy(pl->blob.data() + (pl->off_steps - pl->off_ts), pl->steps.data(), sizeof(ed::DevStep) * nb);
+  if (!pl->idx.empty()) std::memcpy(pl->blob.data() + (pl->off_idx - pl->off_ts), pl->idx.data(), 4 * pl->idx.size());
+  if (pl->ninst) std::memcpy(pl->blob.data() + (pl->off_roots - pl->off_ts), pl->root_rows.data(), 4 * pl->ninst);
+  return ED_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// ABI
+// ------------------------------------------------------------------------------------------------
+extern "C" {
+
+const char *ed_last_error(void) { return g_last_error.c_str(); }
+
+const char *ed_version(void) { return "ed_batch 0.1 sm_100a"; }
+
+ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_type_t *types, int32_t num_types,
+                    const ed_fsm_t *fsm, const ed_plan_opts_t *opts, ed_plan_t **out) {
+  const double t0 = now_us();
+  if (!out) return fail(ED_E_INVALID_ARG, "out == NULL");
+  *out = nullptr;
+  if (num_graphs < 0 || (num_graphs > 0 && !graphs)) return fail(ED_E_INVALID_ARG, "bad graphs");
+  if (num_types <= 0 || !types) return fail(ED_E_INVALID_ARG, "bad types");
+  const int layout = opts ? opts->layout : ED_LAYOUT_SCHEDULE_ORDER;
+  if (layout != ED_LAYOUT_SCHEDULE_ORDER && layout != ED_LAYOUT_PQ) return fail(ED_E_INVALID_ARG, "unknown layout");
+  if (opts)
+    for (int k = 0; k < 7; ++k)
+      if (opts->reserved[k] != 0) return fail(ED_E_INVALID_ARG, "opts.reserved must be 0");
+  ed_plan_t *pl = new (std::nothrow) ed_plan_t();
+  if (!pl) return fail(ED_E_OOM, "out of host memory");
+  pl->types.assign(types, types + num_types);
+  pl->hidden = types[0].hidden;
+  pl->dtype = types[0].dtype;
+  for (int t = 0; t < num_types; ++t) {
+    const ed_op_type_t &ot = types[t];
+    const std::string tag = "type " + std::to_string(t);
+    if (ot.cell_kind < ED_CELL_TREELSTM_LEAF || ot.cell_kind > ED_CELL_LATTICE_WORD) { delete pl; return fail(ED_E_TYPE, tag + ": unknown cell kind"); }
+    if (ot.hidden != pl->hidden || ot.dtype != pl->dtype) { delete pl; return fail(ED_E_TYPE, tag + ": hidden/dtype differ between types"); }
+    if (ot.hidden <= 0) { delete pl; return fail(ED_E_TYPE, tag + ": hidden must be > 0"); }
+    if (ot.dtype != ED_BF16 && ot.dtype != ED_FP32) { delete pl; return fail(ED_E_TYPE, tag + ": unknown dtype"); }
+    if (ot.weight_set < 0 || ot.weight_set >= ed::kMaxWeightSets) { delete pl; return fail(ED_E_TYPE, tag + ": weight_set out of range"); }
+    if (ot.num_slots < 0 || ot.num_slots > 2) { delete pl; return fail(ED_E_TYPE, tag + ": num_slots must be 0..2"); }
+    if ((ot.cell_kind == ED_CELL_LINEAR_OUT || ot.cell_kind == ED_CELL_TAGGER) && (ot.out_dim <= 0 || ot.out_dim > 16)) { delete pl; return fail(ED_E_TYPE, tag + ": out_dim must be 1..16"); }
+    if (ot.dtype == ED_BF16 && ot.hidden % 64 != 0) { delete pl; return fail(ED_E_TYPE, tag + ": bf16 path needs hidden % 64 == 0"); }
+  }
+  ed_status_t st = validate_and_merge(pl, graphs, num_graphs);
+  if (st != ED_OK) { delete pl; return st; }
+  const double t1 = now_us();
+  st = schedule(pl, fsm);
+  if (st != ED_OK) { delete pl; return st; }
+  const double t2 = now_us();
+  if (layout == ED_LAYOUT_PQ) {
+    ed::LayoutInput li{pl->V, &pl->gtype, &pl->in_off, &pl->in_idx, &pl->batch_type, &pl->batch_off, &pl->members,
+                       &pl->types};
+    pl->row_of_node = ed::plan_layout_pq(li);
+    if (pl->row_of_node.size() != static_cast<size_t>(pl->V)) { delete pl; return fail(ED_E_UNSUPPORTED, "PQ layout planner not available"); }
+  } else {
+    pl->row_of_node.assign(pl->V, -1);
+    for (size_t k = 0; k < pl->members.size(); ++k) pl->row_of_node[pl->members[k]] = static_cast<int32_t>(k);
+  }
+  const double t3 = now_us();
+  st = lower(pl);
+  if (st != ED_OK) { delete pl; return st; }
+  pl->sched_us = t2 - t1;
+  pl->layout_us = t3 - t2;
+  pl->plan_us = now_us() - t0;
+  *out = pl;
+  return ED_OK;
+}
+
+ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
+  if (!pl || !o) return fail(ED_E_INVALID_ARG, "null argument");
+  std::memset(o, 0, sizeof(*o));
+  o->num_nodes = pl->V;
+  o->num_instances = pl->ninst;
+  o->num_batches = static_cast<int64_t>(pl->batch_type.size());
+  o->lower_bound = pl->lower_bound;
+  o->num_rows = pl->V + 1;
+  o->hidden = pl->hidden;
+  o->dtype = pl->dtype;
+  o->workspace_bytes = static_cast<int64_t>(pl->ws_bytes);
+  o->contig_operands = pl->contig;
+  o->gather_operands = pl->gather;
+  o->copy_bytes = pl->copy_bytes;
+  o->copy_kernels = pl->copy_kernels;
+  o->off_h = static_cast<int64_t>(pl->off_h);
+  o->off_c = static_cast<int64_t>(pl->off_c);
+  o->off_y = static_cast<int64_t>(pl->off_y);
+  o->y_cols = pl->y_cols;
+  o->off_x = pl->need_x ? static_cast<int64_t>(pl->off_x) : -1;
+  o->off_ts = static_cast<int64_t>(pl->off_ts);
+  o->plan_us = pl->plan_us;
+  o->schedule_us = pl->sched_us;
+  o->layout_us = pl->layout_us;
+  return ED_OK;
+}
+
+ed_status_t ed_plan_get_schedule(const ed_plan_t *pl, int32_t *bt, int32_t *bo, int32_t *mem) {
+  if (!pl || !bt || !bo || !mem) return fail(ED_E_INVALID_ARG, "null argument");
+  std::copy(pl->batch_type.begin(), pl->batch_type.end(), bt);
+  std::copy(pl->batch_off.begin(), pl->batch_off.end(), bo);
+  std::copy(pl->members.begin(), pl->members.end(), mem);
+  return ED_OK;
+}
+
+ed_status_t ed_plan_get_layout(const ed_plan_t *pl, int32_t *row) {
+  if (!pl || !row) return fail(ED_E_INVALID_ARG, "null argument");
+  std::copy(pl->row_of_node.begin(), pl->row_of_node.end(), row);
+  return ED_OK;
+}
+
+ed_status_t ed_plan_get_slot_modes(const ed_plan_t *pl, int32_t *modes) {
+  if (!pl || !modes) return fail(ED_E_INVALID_ARG, "null argument");
+  std::copy(pl->slot_modes.begin(), pl->slot_modes.end(), modes);
+  return ED_OK;
+}
+
+void ed_plan_destroy(ed_plan_t *pl) {
+  if (!pl) return;
+  if (pl->pinned) cudaFreeHost(pl->pinned);
+  delete pl;
+}
+
+int64_t ed_packed_bytes(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which) {
+  return ed::packed_bytes(cell_kind, hidden, out_dim, dtype, which);
+}
+
+ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which,
+                            const float *logical_dev, void *packed_dev, void *stream) {
+  if (!logical_dev || !packed_dev) return fail(ED_E_INVALID_ARG, "null pointer");
+  if (cell_kind < ED_CELL_TREELSTM_LEAF || cell_kind > ED_CELL_LATTICE_WORD) return fail(ED_E_TYPE, "unknown cell kind");
+  int sms = 0, major = 0, minor = 0;
+  int e = ed::device_check(&sms, &major, &minor);
+  if (e) return fail(ED_E_CUDA, std::string("cuda: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  if (major != 10 || minor != 0) return fail(ED_E_UNSUPPORTED, "device is not sm_100");
+  e = ed::launch_pack(cell_kind, hidden, out_dim, dtype, which, logical_dev, packed_dev, stream);
+  if (e) return fail(ED_E_CUDA, std::string("pack: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  return ED_OK;
+}
+
+int32_t ed_execute_launch_count(const ed_plan_t *pl) { return pl ? 1 : 0; }
+
+ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, void *ws, size_t ws_bytes,
+                       void *stream) {
+  if (!pl || !w) return fail(ED_E_INVALID_ARG, "null argument");
+  if (!ws || (reinterpret_cast<uintptr_t>(ws) & 1023) != 0) return fail(ED_E_WORKSPACE, "workspace null or not 1024-aligned");
+  if (ws_bytes < pl->ws_bytes) return fail(ED_E_WORKSPACE, "workspace too small: need " + std::to_string(pl->ws_bytes));
+  if (w->num_sets <= 0 || w->num_sets > ed::kMaxWeightSets || !w->sets) return fail(ED_E_INVALID_ARG, "bad weights");
+  for (const auto &ot : pl->types)
+    if (ot.weight_set >= w->num_sets) return fail(ED_E_INVALID_ARG, "weight set missing");
+  int sms = 0, major = 0, minor = 0;
+  int e = ed::device_check(&sms, &major, &minor);
+  if (e) return fail(ED_E_CUDA, std::string("cuda: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  if (major != 10 || minor != 0) return fail(ED_E_UNSUPPORTED, "device is not sm_100 (sm_" + std::to_string(major * 10 + minor) + ")");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t *base = static_cast<uint8_t *>(ws);
+  if (pl->uploaded_ws != ws) {
+    if (!pl->pinned) {
+      cudaError_t ce = cudaMallocHost(&pl->pinned, pl->blob.size() > 0 ? pl->blob.size() : 1);
+      if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(ce));
+      std::memcpy(pl->pinned, pl->blob.data(), pl->blob.size());
+    }
+    cudaError_t ce = cudaMemcpyAsync(base + pl->off_ts, pl->pinned, pl->blob.size(), cudaMemcpyHostToDevice, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_bar, 0, pl->off_ts - pl->off_bar, s);  // barrier flags
+    if (ce == cudaSuccess) {
+      const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
+      ce = cudaMemsetAsync(base + pl->off_h + elt * pl->V * pl->hidden, 0, elt * pl->hidden, s);
+      if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_c + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
+      if (ce == cudaSuccess && pl->need_x)
+        ce = cudaMemsetAsync(base + pl->off_x + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
+    }
+    if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
+    pl->uploaded_ws = ws;
+  }
+  if (pl->grid == 0) {
+    e = ed::persistent_grid(pl->dtype, &pl->grid);
+    if (e) return fail(ED_E_CUDA, std::string("occupancy: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  }
+  ed::KParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.steps = reinterpret_cast<const ed::DevStep *>(base + pl->off_steps);
+  p.idx = reinterpret_cast<const int32_t *>(base + pl->off_idx);
+  p.root_rows = reinterpret_cast<const int32_t *>(base + pl->off_roots);
+  p.H = base + pl->off_h;
+  p.C = reinterpret_cast<float *>(base + pl->off_c);
+  p.Y = reinterpret_cast<float *>(base + pl->off_y);
+  p.X = pl->need_x ? reinterpret_cast<float *>(base + pl->off_x) : nullptr;
+  p.bar = reinterpret_cast<unsigned int *>(base + pl->off_bar);
+  p.ts = reinterpret_cast<unsigned long long *>(base + pl->off_ts);
+  p.out_root = io ? io->out_root : nullptr;
+  p.trace = io ? reinterpret_cast<unsigned long long *>(io->trace) : nullptr;
+  p.num_steps = static_cast<int32_t>(pl->batch_type.size());
+  p.hidden = pl->hidden;
+  p.rows = static_cast<int32_t>(pl->V + 1);
+  p.zero_row = static_cast<int32_t>(pl->V);
+  p.ycols = static_cast<int32_t>(pl->y_cols);
+  p.num_inst = pl->ninst;
+  p.root_wset = pl->types[0].weight_set;
+  p.launch_id = (++pl->launches) & 0xFFFFu;
+  if (p.launch_id == 0) p.launch_id = (++pl->launches) & 0xFFFFu;
+  for (int k = 0; k < w->num_sets; ++k) {
+    const ed_weight_set_t &ws_ = w->sets[k];
+    p.w[k] = ed::DevWeightSet{ws_.W, ws_.b, ws_.W2, ws_.b2, ws_.emb, ws_.emb2, ws_.mat, ws_.emb_rows, ws_.emb2_rows};
+  }
+  if (pl->dtype == ED_BF16) {
+    if (!encode_rows(&p.tm_h1, p.H, pl->V + 1, pl->hidden, 1) ||
+        !encode_rows(&p.tm_h128, p.H, pl->V + 1, pl->hidden, 128))
+      return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for the H buffer");
+    for (int k = 0; k < w->num_sets; ++k)
+      if (w->sets[k].emb && w->sets[k].emb_rows > 0 &&
+          !encode_rows(&p.tm_emb1[k], w->sets[k].emb, w->sets[k].emb_rows, pl->hidden, 1))
+        return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for an embedding table");
+  }
+  e = ed::launch_persistent(p, pl->dtype, pl->grid, stream);
+  if (e) return fail(ED_E_CUDA, std::string("launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  return ED_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// Internal definitions shared by the host planner (ed_batch.cpp) and the device code
+// (ed_kernels.cu).  Not part of the public ABI (include/ed_batch.h is).
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+#include "ed_batch.h"
+
+namespace ed {
+
+constexpr int kMaxWeightSets = 8;
+constexpr int kMaxSlotsDev = 2;   // fixed slots the device reads (all cells have <= 2)
+
+// One batch of the schedule as the persistent kernel sees it (SoA-friendly 64 B record).
+// Slot j of member i (position i = ascending result row):
+//   mode[j] == 1 (CONTIG): entry = arg[j] + i             (one contiguous aligned block)
+//   mode[j] == 0 (GATHER): entry = idx[arg[j] + i]
+// An entry >= 0 is a row of the H/C/X buffers (the zero row for ED_ZERO_INPUT); an entry < 0 is
+// an external id (-1 - id) read from the weight set's embedding table.
+struct DevStep {
+  int32_t cell;       // ED_CELL_*
+  int32_t m;          // batch size
+  int32_t out_row0;   // results occupy rows out_row0 .. out_row0 + m - 1 (always contiguous)
+  int32_t wset;       // weight set
+  int32_t mode[kMaxSlotsDev];
+  int32_t arg[kMaxSlotsDev];
+  int32_t ext_off;    // idx offset of the per-member ext token ids, -1 if none
+  int32_t var_off;    // idx offset of m+1 absolute offsets of variadic input lists, -1 if none
+  int32_t units;      // UMMA path: hidden units per column tile (multiple of 16)
+  int32_t n_col_tiles;// UMMA path: hidden / units
+  int32_t gates;      // G: gate blocks of the main contraction
+  int32_t nslots;     // fixed slots present
+  int32_t pad[2];
+};
+static_assert(sizeof(DevStep) == 64, "DevStep must be 64 bytes");
+
+struct DevWeightSet {
+  const void *W;
+  const float *b;
+  const void *W2;
+  const float *b2;
+  const void *emb;
+  const void *emb2;
+  const void *mat;
+  int32_t emb_rows;
+  int32_t emb2_rows;
+};
+
+// Kernel parameters (passed as __grid_constant__ so the TMA descriptors below are addressable).
+struct alignas(64) KParams {
+  CUtensorMap tm_h1;                     // H rows, box {64 cols, 1 row}: gather4 / single rows
+  CUtensorMap tm_h128;                   // H rows, box {64 cols, 128 rows}: contiguous blocks
+  CUtensorMap tm_emb1[kMaxWeightSets];   // embedding tables, box {64, 1}
+  const DevStep *steps;
+  const int32_t *idx;
+  const int32_t *root_rows;   // per instance: row (>= 0) or external id (-1 - id)
+  void *H;                    // [rows x hidden] bf16 or fp32
+  float *C;                   // [rows x hidden]
+  float *Y;                   // [rows x ycols]
+  float *X;                   // [rows x hidden] (lattice link gates) or null
+  unsigned int *bar;          // grid barrier counter (zeroed before launch)
+  unsigned long long *ts;     // [num_steps + 1]
+  void *out_root;             // [num_inst x hidden] or null
+  unsigned long long *trace;  // [num_steps x 8] phase stamps of CTA 0, or null
+  int32_t num_steps;
+  int32_t hidden;
+  int32_t rows;
+  int32_t zero_row;
+  int32_t ycols;
+  int32_t num_inst;
+  int32_t root_wset;
+  uint32_t launch_id;          // distinguishes barrier flags of successive launches
+  int32_t pad2[2];
+  DevWeightSet w[kMaxWeightSets];
+};
+
+// Gates of the main contraction per cell kind (0: not a single-GEMM cell).
+inline int cell_gates(int cell) {
+  switch (cell) {
+    case ED_CELL_TREELSTM_LEAF: return 3;
+    case ED_CELL_TREELSTM_INTERNAL: return 5;
+    case ED_CELL_TREEGRU_LEAF: return 2;
+    case ED_CELL_TREEGRU_INTERNAL: return 5;
+    case ED_CELL_TREEFC_INTERNAL: return 1;
+    case ED_CELL_LSTM: return 4;
+    case ED_CELL_LATTICE_CHAR: return 4;
+    case ED_CELL_LATTICE_WORD: return 3;
+    case ED_CELL_TAGGER: return 1;
+    case ED_CELL_MVRNN_INTERNAL: return 1;
+    default: return 0;
+  }
+}
+
+// Hidden units per column tile on the bf16 tensor-core path (N tile = gates * units <= 256).
+// Fixed per cell kind so that host tiling and the device epilogue templates agree.
+inline int cell_units(int cell) {
+  switch (cell) {
+    case ED_CELL_TREELSTM_LEAF: return 64;      // N = 192
+    case ED_CELL_TREELSTM_INTERNAL: return 32;  // N = 160
+    case ED_CELL_TREEGRU_LEAF: return 64;       // N = 128
+    case ED_CELL_TREEGRU_INTERNAL: return 32;   // N = 160
+    case ED_CELL_TREEFC_INTERNAL: return 64;    // N = 64
+    case ED_CELL_LSTM: return 64;               // N = 256
+    case ED_CELL_LATTICE_CHAR: return 64;       // N = 256
+    default: return 0;
+  }
+}
+
+// K segments (each of width hidden) of the main contraction.
+inline int cell_segments(int cell) {
+  switch (cell) {
+    case ED_CELL_TREELSTM_LEAF:
+    case ED_CELL_TREEGRU_LEAF:
+    case ED_CELL_LINEAR_OUT: return 1;
+    default: return 2;
+  }
+}
+
+// Launch entry points implemented in ed_kernels.cu (return cudaError_t as int).
+int launch_persistent(const KParams &p, int dtype, int grid, void *stream);
+int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const float *src, void *dst,
+                void *stream);
+int64_t packed_bytes(int cell, int hidden, int out_dim, int dtype, int which);
+int device_check(int *sm_count, int *major, int *minor);
+int persistent_grid(int dtype, int *grid);
+
+}  // namespace ed

@@ -1,0 +1,988 @@
+// ed_kernels.cu — device side of the ED-Batch hot path for sm_100a (B200).
+//
+// One persistent cooperative kernel walks the whole FSM batch schedule (PAPER Alg. 1,
+// P:75-87): for every batch ("step") it reads operand rows (gathered by index, or one contiguous
+// block where the layout plan made them adjacent), runs the cell's dense contraction,
+// applies the fused gate epilogue and stores the results as one contiguous row block; a grid-wide
+// barrier separates dependent steps, replacing the per-batch kernel launches of the paper's
+// DyNet executor.
+//
+//   bf16 path (ed_persistent_bf16): single-GEMM cells on the 5th-gen tensor cores —
+//     warps 0-3  epilogue: tcgen05.ld TMEM -> registers, gates in fp32, vector stores
+//     warp  4    MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128)
+//     warp  5    weight loader: cp.async.bulk of pre-swizzled weight tiles (complete_tx)
+//     warps 6-7  operand loaders: TMA 128-row box for CONTIG operands, 16 B cp.async row gathers
+//                otherwise, into 128B-swizzled A tiles
+//     4-stage smem ring (mbarrier full/empty), 2 TMEM accumulators (2 x 256 columns).
+//     Narrow cells (output linear, N = C) run as a warp-per-row SIMT phase (HBM-bound).
+//   fp32 path (ed_persistent_f32): FFMA SIMT for every cell (1e-4 parity path; single-pass TF32
+//     and approximate transcendentals cannot meet 1e-4).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ed_internal.h"
+
+namespace ed {
+
+// ------------------------------------------------------------------------------------------------
+// constants of the bf16 tensor-core engine
+// ------------------------------------------------------------------------------------------------
+constexpr int kThreads = 256;
+constexpr int kStages = 4;
+constexpr int kTileM = 128;
+constexpr int kChunkK = 64;                  // bf16 elements per 128 B swizzle row
+constexpr int kAStage = kTileM * 128;        // 16 KB
+constexpr int kBStage = 256 * 128;           // 32 KB (N tile <= 256)
+constexpr int kStageBytes = kAStage + kBStage;
+constexpr int kRowTab = kTileM * 2 * 8;      // row pointers per tile (2 segments)
+constexpr int kBiasBytes = 5 * 1024 * 4;          // G * h fp32 (h <= 1024)
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kBiasBytes + 256;
+constexpr int kEpiThreads = 128;
+constexpr int kLag = 3;  // cp.async groups in flight before a stage is released (< kStages)
+
+// ------------------------------------------------------------------------------------------------
+// PTX helpers
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar), ok = 0, spins = 0;
+  do {
+    if (++spins > (1u << 30)) __trap();  // watchdog: a lost arrival must not hang the GPU
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA: one box {64 cols, box rows} of a 2-D bf16 tensor at (col, row) -> smem, complete_tx on bar
+__device__ __forceinline__ void tma_row_box(void *dst, const CUtensorMap *m, int col, int row, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(m), "r"(col), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA tile::gather4: 4 rows (r0..r3) x 64 cols at col -> 4 consecutive 128 B smem rows (128B swizzle)
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *m, int col, int r0, int r1, int r2, int r3,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+// Instruction descriptor kind::f16: D f32, A/B bf16, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(kTileM >> 4) << 24);
+}
+
+// Grid-wide barrier between dependent batches.  Arrivals: one acq_rel atomic per CTA on a counter;
+// the last arriver publishes the epoch to a per-CTA flag (one 256 B line per CTA, so the waiting
+// CTAs poll 148 different L2 lines instead of hammering one).  Flag value = launch_id << 16 | epoch,
+// so flags left by earlier launches never match.
+__device__ __forceinline__ void grid_sync(unsigned int *bar, unsigned int launch_id, unsigned int &epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * gridDim.x;
+    const unsigned int want = (launch_id << 16) | epoch;
+    unsigned int *flags = bar + 64;
+    __threadfence();
+    unsigned int old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == target - 1) {
+      __threadfence();  // one release fence, then relaxed flag stores (release pattern)
+      for (unsigned int c = 0; c < gridDim.x; ++c)
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + c * 64), "r"(want) : "memory");
+    } else {
+      unsigned int v, spins = 0;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + blockIdx.x * 64) : "memory");
+        if (v == want) break;
+        if (++spins > (1u << 26)) __trap();
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// optional phase trace of CTA 0 (profiling aid)
+#define ED_TRACE(p, s, k, first) \
+  do { if ((p).trace && blockIdx.x == 0 && (first)) (p).trace[(s) * 64 + (k)] = globaltimer(); } while (0)
+
+// ------------------------------------------------------------------------------------------------
+// cell math — one hidden unit, fp32
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ int cell_segments_dev(int cell) {
+  return (cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF || cell == ED_CELL_LINEAR_OUT) ? 1 : 2;
+}
+
+__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+// bf16 path: MUFU tanh.approx (rel. err ~2^-11, below the bf16 rounding of h, 2^-9)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigm_fast(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
+// activations by storage type: fp32 path accurate (1e-4 parity), bf16 path MUFU approximations
+template <typename T> __device__ __forceinline__ float act_sig(float x) { return sigm_fast(x); }
+template <> __device__ __forceinline__ float act_sig<float>(float x) { return sigm(x); }
+template <typename T> __device__ __forceinline__ float act_tanh(float x) { return tanh_fast(x); }
+template <> __device__ __forceinline__ float act_tanh<float>(float x) { return tanhf(x); }
+template <typename T> __device__ __forceinline__ float act_exp(float x) { return __expf(x); }
+template <> __device__ __forceinline__ float act_exp<float>(float x) { return expf(x); }
+
+__device__ __forceinline__ int slot_entry(const DevStep &st, const int32_t *idx, int j, int i) {
+  return st.mode[j] ? st.arg[j] + i : __ldg(idx + st.arg[j] + i);
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Pointer to the h-vector an operand entry refers to (row of H, or an external embedding row).
+template <typename T>
+__device__ __forceinline__ const T *entry_row(const KParams &p, const DevWeightSet &w, int e, bool second) {
+  if (e >= 0) return static_cast<const T *>(p.H) + static_cast<size_t>(e) * p.hidden;
+  const int id = -1 - e;
+  const T *tab = static_cast<const T *>(second ? w.emb2 : w.emb);
+  return tab + static_cast<size_t>(id) * p.hidden;
+}
+
+// K segment s (width hidden) of member i's A operand.
+template <typename T>
+__device__ __forceinline__ const T *segment_row(const KParams &p, const DevStep &st, int s, int i) {
+  const DevWeightSet &w = p.w[st.wset];
+  const int cell = st.cell;
+  const bool ext_first = (cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF ||
+                          cell == ED_CELL_LSTM || cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD);
+  if (ext_first) {
+    if (s == 0) {
+      const int tok = __ldg(p.idx + st.ext_off + i);
+      return static_cast<const T *>(w.emb) + static_cast<size_t>(tok) * p.hidden;
+    }
+    return entry_row<T>(p, w, slot_entry(st, p.idx, 0, i), false);
+  }
+  return entry_row<T>(p, w, slot_entry(st, p.idx, s, i), false);
+}
+
+__device__ __forceinline__ bool ext_first_cell(int cell) {
+  return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF || cell == ED_CELL_LSTM ||
+         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD;
+}
+// Operand entry of K segment s for member i: >= 0 row of H; < 0 embedding row (-1 - id).
+__device__ __forceinline__ int segment_entry(const KParams &p, const DevStep &st, int s, int i) {
+  if (ext_first_cell(st.cell)) {
+    if (s == 0) return -1 - __ldg(p.idx + st.ext_off + i);
+    return slot_entry(st, p.idx, 0, i);
+  }
+  return slot_entry(st, p.idx, s, i);
+}
+// Whether K segment s is one contiguous block of H rows (layout plan made it adjacent + aligned).
+__device__ __forceinline__ bool segment_contig(const DevStep &st, int s, int *base) {
+  int slot = s;
+  if (ext_first_cell(st.cell)) {
+    if (s == 0) return false;
+    slot = 0;
+  }
+  *base = st.arg[slot];
+  return st.mode[slot] != 0;
+}
+
+__device__ __forceinline__ float c_of(const KParams &p, int e, int j) {
+  return e >= 0 ? __ldcg(p.C + static_cast<size_t>(e) * p.hidden + j) : 0.0f;
+}
+
+// Scalar epilogue for one (member i, unit j) given the gate pre-activations z[] (bias included).
+template <typename T>
+__device__ __forceinline__ void cell_epilogue(const KParams &p, const DevStep &st, int i, int j, const float *z) {
+  const int h = p.hidden;
+  const size_t orow = static_cast<size_t>(st.out_row0 + i);
+  T *H = static_cast<T *>(p.H);
+  float c = 0.f, hv = 0.f;
+  bool has_c = true;
+  switch (st.cell) {
+    case ED_CELL_TREELSTM_LEAF:  // [i;o;u]
+      c = act_sig<T>(z[0]) * act_tanh<T>(z[2]);
+      hv = act_sig<T>(z[1]) * act_tanh<T>(c);
+      break;
+    case ED_CELL_TREELSTM_INTERNAL: {  // [i;f_l;f_r;o;u]
+      const int el = slot_entry(st, p.idx, 0, i), er = slot_entry(st, p.idx, 1, i);
+      c = act_sig<T>(z[0]) * act_tanh<T>(z[4]) + act_sig<T>(z[1]) * c_of(p, el, j) + act_sig<T>(z[2]) * c_of(p, er, j);
+      hv = act_sig<T>(z[3]) * act_tanh<T>(c);
+      break;
+    }
+    case ED_CELL_TREEGRU_LEAF:  // [z;n]
+      hv = (1.f - act_sig<T>(z[0])) * act_tanh<T>(z[1]);
+      has_c = false;
+      break;
+    case ED_CELL_TREEGRU_INTERNAL: {  // [z;r_l;r_r;a_l;a_r]
+      const int el = slot_entry(st, p.idx, 0, i), er = slot_entry(st, p.idx, 1, i);
+      const DevWeightSet &w = p.w[st.wset];
+      const float hl = to_f<T>(entry_row<T>(p, w, el, false)[j]);
+      const float hr = to_f<T>(entry_row<T>(p, w, er, false)[j]);
+      const float n = act_tanh<T>(act_sig<T>(z[1]) * z[3] + act_sig<T>(z[2]) * z[4]);
+      const float zz = act_sig<T>(z[0]);
+      hv = (1.f - zz) * n + zz * (hl + hr);
+      has_c = false;
+      break;
+    }
+    case ED_CELL_TREEFC_INTERNAL:
+      hv = act_tanh<T>(z[0]);
+      has_c = false;
+      break;
+    case ED_CELL_LSTM: {  // [i;f;g;o]
+      const int ep = slot_entry(st, p.idx, 0, i);
+      c = act_sig<T>(z[1]) * c_of(p, ep, j) + act_sig<T>(z[0]) * act_tanh<T>(z[2]);
+      hv = act_sig<T>(z[3]) * act_tanh<T>(c);
+      break;
+    }
+    case ED_CELL_LATTICE_CHAR: {  // [i;f;o;g]; variadic words: softmax over {s(i)} U {l_w}
+      const int ep = slot_entry(st, p.idx, 0, i);
+      const int beg = __ldg(p.idx + st.var_off + i), end = __ldg(p.idx + st.var_off + i + 1);
+      const float si = act_sig<T>(z[0]), tg = act_tanh<T>(z[3]);
+      if (beg == end) {
+        c = act_sig<T>(z[1]) * c_of(p, ep, j) + si * tg;
+      } else {
+        const float ei = act_exp<T>(si);
+        float den = ei, num = ei * tg;
+        for (int k = beg; k < end; ++k) {
+          const int wr = __ldg(p.idx + k);
+          const float el = act_exp<T>(__ldcg(p.X + static_cast<size_t>(wr) * h + j));
+          den += el;
+          num += el * __ldcg(p.C + static_cast<size_t>(wr) * h + j);
+        }
+        c = num / den;
+      }
+      hv = act_sig<T>(z[2]) * act_tanh<T>(c);
+      break;
+    }
+    default:
+      return;
+  }
+  H[orow * h + j] = from_f<T>(hv);
+  if (has_c) p.C[orow * h + j] = c;
+}
+
+// ------------------------------------------------------------------------------------------------
+// SIMT engine (fp32 path for every cell; bf16 path for the cells without a tensor-core variant)
+// Weights: Wt[k][n] (transposed logical [G*h, K]), element type T.
+// ------------------------------------------------------------------------------------------------
+template <typename T>
+__device__ void simt_gemm_step(const KParams &p, const DevStep &st) {
+  const int h = p.hidden, G = st.gates, NS = cell_segments_dev(st.cell);
+  const DevWeightSet &w = p.w[st.wset];
+  const T *Wt = static_cast<const T *>(w.W);
+  const int lane = threadIdx.x & 31;
+  const int nub = (h + 31) / 32;
+  const long tasks = static_cast<long>(st.m) * nub;
+  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  const int ldw = G * h;
+  for (long task = gw; task < tasks; task += nw) {
+    const int i = static_cast<int>(task / nub);
+    const int j = static_cast<int>(task % nub) * 32 + lane;
+    const bool act = j < h;
+    const int jj = act ? j : 0;
+    float z[5];
+#pragma unroll
+    for (int g = 0; g < 5; ++g) z[g] = (g < G) ? w.b[g * h + jj] : 0.f;
+    for (int s = 0; s < NS; ++s) {
+      const T *a = segment_row<T>(p, st, s, i);
+      const T *wk = Wt + static_cast<size_t>(s) * h * ldw + jj;
+      for (int k = 0; k < h; ++k) {
+        const float av = to_f<T>(a[k]);
+#pragma unroll
+        for (int g = 0; g < 5; ++g)
+          if (g < G) z[g] = fmaf(av, to_f<T>(wk[static_cast<size_t>(k) * ldw + g * h]), z[g]);
+      }
+    }
+    if (act) cell_epilogue<T>(p, st, i, j, z);
+  }
+}
+
+
+// Output linear O (y = W h + b, fp32 logits): warp per row, W fp32 [C x h].
+template <typename T>
+__device__ void simt_linear_out(const KParams &p, const DevStep &st) {
+  const int h = p.hidden;
+  const DevWeightSet &w = p.w[st.wset];
+  const float *W = static_cast<const float *>(w.W);
+  const int C = p.ycols;
+  const int lane = threadIdx.x & 31;
+  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  for (long i = gw; i < st.m; i += nw) {
+    const T *a = entry_row<T>(p, w, slot_entry(st, p.idx, 0, static_cast<int>(i)), false);
+    float acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.f;
+    for (int k = lane; k < h; k += 32) {
+      const float av = to_f<T>(a[k]);
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < C) acc[c] = fmaf(av, __ldg(W + c * h + k), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      float v = acc[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[c] = v;
+    }
+    if (lane == 0) {
+      float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
+      for (int c = 0; c < C; ++c) y[c] = acc[c] + w.b[c];
+    }
+  }
+}
+
+// bf16 variant (HBM-bound): W staged in shared memory as [h][C] fp32, each warp streams two rows
+// at a time with 16 B loads (lane owns 8-element chunks lane, lane+32, ...), h % 64 == 0.
+__device__ void simt_linear_out_bf16(const KParams &p, const DevStep &st, float *smem_w) {
+  const int h = p.hidden, C = p.ycols;
+  const DevWeightSet &w = p.w[st.wset];
+  const float *W = static_cast<const float *>(w.W);
+  for (int q = threadIdx.x; q < C * h; q += blockDim.x) smem_w[q] = W[q];  // [c][k]
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nch = h / 8;                 // 16 B chunks per row
+  const int cpl = (nch + 31) / 32;       // chunks per lane (<= 4 for h <= 1024)
+  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  for (long i0 = gw * 2; i0 < st.m; i0 += nw * 2) {
+    uint4 v[2][4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const long i = i0 + r;
+      const __nv_bfloat16 *a = nullptr;
+      if (i < st.m) a = entry_row<__nv_bfloat16>(p, w, slot_entry(st, p.idx, 0, static_cast<int>(i)), false);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ch = lane + 32 * q;
+        v[r][q] = (a != nullptr && q < cpl && ch < nch) ? __ldcg(reinterpret_cast<const uint4 *>(a) + ch)
+                                                         : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float acc[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc[c] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ch = lane + 32 * q;
+        if (q >= cpl || ch >= nch) continue;
+        const __nv_bfloat16 *e = reinterpret_cast<const __nv_bfloat16 *>(&v[r][q]);
+        float av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = __bfloat162float(e[u]);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          if (c >= C) break;
+          const float4 w0 = *reinterpret_cast<const float4 *>(smem_w + c * h + ch * 8);
+          const float4 w1 = *reinterpret_cast<const float4 *>(smem_w + c * h + ch * 8 + 4);
+          acc[c] = fmaf(av[0], w0.x, fmaf(av[1], w0.y, fmaf(av[2], w0.z, fmaf(av[3], w0.w, acc[c]))));
+          acc[c] = fmaf(av[4], w1.x, fmaf(av[5], w1.y, fmaf(av[6], w1.z, fmaf(av[7], w1.w, acc[c]))));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        float x = acc[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        acc[c] = x;
+      }
+      const long i = i0 + r;
+      if (lane == 0 && i < st.m) {
+        float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
+        for (int c = 0; c < C; ++c) y[c] = acc[c] + w.b[c];
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ void collect_roots(const KParams &p) {
+  if (p.out_root == nullptr) return;
+  const int h = p.hidden;
+  T *out = static_cast<T *>(p.out_root);
+  const long total = static_cast<long>(p.num_inst) * h;
+  for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int inst = static_cast<int>(q / h), j = static_cast<int>(q % h);
+    const int r = p.root_rows[inst];
+    out[q] = entry_row<T>(p, p.w[p.root_wset], r, false)[j];
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// fp32 persistent kernel: all SIMT
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) ed_persistent_f32(const __grid_constant__ KParams p) {
+  unsigned int epoch = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[0] = globaltimer();
+  for (int s = 0; s < p.num_steps; ++s) {
+    const DevStep st = p.steps[s];
+    if (st.cell == ED_CELL_LINEAR_OUT)
+      simt_linear_out<float>(p, st);
+    else
+      simt_gemm_step<float>(p, st);
+    grid_sync(p.bar, p.launch_id, epoch);
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[s + 1] = globaltimer();
+  }
+  collect_roots<float>(p);
+}
+
+// ------------------------------------------------------------------------------------------------
+// bf16 persistent kernel: tcgen05 tensor-core engine
+// ------------------------------------------------------------------------------------------------
+struct Pipe {
+  uint32_t it = 0;  // global K-chunk counter (stage = it % kStages, phase = (it / kStages) & 1)
+  uint32_t ti = 0;  // global tile counter (accumulator = ti & 1)
+};
+
+__device__ __forceinline__ bool is_umma_cell(int cell) {
+  return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
+         cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
+         cell == ED_CELL_LATTICE_CHAR;
+}
+
+// Per-cell configuration of the tensor-core epilogue: G gates, U units per column tile (must
+// match ed::cell_units), NAUX fp32 rows of C prefetched per member (children / previous state).
+template <int CELL> struct CellCfg;
+template <> struct CellCfg<ED_CELL_TREELSTM_LEAF> { static constexpr int G = 3, U = 64, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREELSTM_INTERNAL> { static constexpr int G = 5, U = 32, NAUX = 2; };
+template <> struct CellCfg<ED_CELL_TREEGRU_LEAF> { static constexpr int G = 2, U = 64, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREEGRU_INTERNAL> { static constexpr int G = 5, U = 32, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1, U = 64, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_LSTM> { static constexpr int G = 4, U = 64, NAUX = 1; };
+template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NAUX = 1; };
+
+__device__ __forceinline__ float f4get(const float4 &v, int k) {
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+// Epilogue of one 128 x (G*U) tile for thread r (= TMEM lane = tile row): prefetch the child /
+// previous-state C rows, wait for the accumulator, then per 16 units: tcgen05.ld -> gates (fp32,
+// MUFU tanh.approx) -> bf16 h and fp32 c vector stores.  Bias comes from shared memory.
+template <int CELL>
+__device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
+                                              uint32_t parity, int row_tile, int col_tile, int r,
+                                              const float *sbias) {
+  using CC = CellCfg<CELL>;
+  constexpr int G = CC::G, U = CC::U, NA = CC::NAUX, QPR = U / 4;
+  const int h = p.hidden;
+  const int i = row_tile * kTileM + r;
+  const bool valid = i < st.m;
+  const int jb = col_tile * U;
+  int e0 = p.zero_row, e1 = p.zero_row;
+  if (valid && st.nslots > 0) e0 = slot_entry(st, p.idx, 0, i);
+  if (valid && st.nslots > 1) e1 = slot_entry(st, p.idx, 1, i);
+  float4 aux[NA > 0 ? NA * QPR : 1];
+#pragma unroll
+  for (int q = 0; q < NA * QPR; ++q) {
+    const int row = q < QPR ? e0 : e1;
+    aux[q] = row >= 0 ? __ldcg(reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(row) * h + jb) + (q % QPR))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  mbar_wait(tfull_bar, parity);
+  tc_fence_after();
+  __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
+  const size_t orow = static_cast<size_t>(st.out_row0 + (valid ? i : 0));
+#pragma unroll
+  for (int gq = 0; gq < U / 16; ++gq) {
+    float z[G][16];
+#pragma unroll
+    for (int g = 0; g < G; ++g) tmem_ld16(tacc + static_cast<uint32_t>(gq * G * 16 + g * 16), z[g]);
+    tmem_wait_ld();
+    if (!valid) continue;
+    const int j0 = jb + gq * 16;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) z[g][k] += sbias[g * h + j0 + k];
+    float hv[16], cv[16];
+    bool has_c = true, done = false;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int qa = gq * 4 + (k >> 2), ka = k & 3;
+      if constexpr (CELL == ED_CELL_TREELSTM_LEAF) {  // [i;o;u]
+        cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
+        hv[k] = sigm_fast(z[1 % G][k]) * tanh_fast(cv[k]);
+      } else if constexpr (CELL == ED_CELL_TREELSTM_INTERNAL) {  // [i;f_l;f_r;o;u]
+        const float cl = f4get(aux[qa % (NA * QPR)], ka), cr = f4get(aux[(QPR + qa) % (NA * QPR)], ka);
+        cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[4 % G][k]) + sigm_fast(z[1 % G][k]) * cl +
+                sigm_fast(z[2 % G][k]) * cr;
+        hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
+      } else if constexpr (CELL == ED_CELL_LSTM) {  // [i;f;g;o]
+        const float cp = f4get(aux[qa % (NA * QPR)], ka);
+        cv[k] = sigm_fast(z[1 % G][k]) * cp + sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
+        hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
+      } else if constexpr (CELL == ED_CELL_TREEGRU_LEAF) {  // [z;n]
+        hv[k] = (1.f - sigm_fast(z[0][k])) * tanh_fast(z[1 % G][k]);
+        has_c = false;
+      } else if constexpr (CELL == ED_CELL_TREEFC_INTERNAL) {
+        hv[k] = tanh_fast(z[0][k]);
+        has_c = false;
+      } else {
+        // TreeGRU internal / lattice char: scalar path shared with the SIMT engine
+        float zz[5];
+#pragma unroll
+        for (int g = 0; g < 5; ++g) zz[g] = z[g % G][k];
+        cell_epilogue<__nv_bfloat16>(p, st, i, j0 + k, zz);
+        done = true;
+      }
+    }
+    if (done) continue;
+    uint32_t packed[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      __nv_bfloat162 t = __floats2bfloat162_rn(hv[2 * k], hv[2 * k + 1]);
+      packed[k] = *reinterpret_cast<uint32_t *>(&t);
+    }
+    uint4 *hd = reinterpret_cast<uint4 *>(H + orow * h + j0);
+    hd[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    hd[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    if (has_c) {
+      float4 *cd = reinterpret_cast<float4 *>(p.C + orow * h + j0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cd[q] = make_float4(cv[4 * q], cv[4 * q + 1], cv[4 * q + 2], cv[4 * q + 3]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_constant__ KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *stages = smem;
+  const void **rowtab = reinterpret_cast<const void **>(smem + kStages * kStageBytes);  // [2][128][2] row ptrs
+  float *sbias = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + 2 * kRowTab + kBiasBytes);
+  uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = bars + 2 * kStages + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 4);  // A TMA-or-nothing arrival + 2 cp.async warps + B loader (expect_tx)
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, kEpiThreads);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  unsigned int epoch = 0;
+  Pipe pipe;
+  uint32_t tab_tile = 0;        // loader threads: row-table buffer toggle
+  uint32_t cp_pending = 0;      // cp.async warp: committed groups not yet released
+  if (blockIdx.x == 0 && tid == 0) p.ts[0] = globaltimer();
+
+  for (int s = 0; s < p.num_steps; ++s) {
+    const DevStep st = p.steps[s];
+    ED_TRACE(p, s, 0, tid == 0);
+    if (!is_umma_cell(st.cell)) {
+      if (st.cell == ED_CELL_LINEAR_OUT) simt_linear_out_bf16(p, st, reinterpret_cast<float *>(stages));
+      else simt_gemm_step<__nv_bfloat16>(p, st);
+    } else {
+      const int h = p.hidden;
+      const int ncols = st.gates * st.units;
+      const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
+      const int mt = (st.m + kTileM - 1) / kTileM;
+      const int T = mt * st.n_col_tiles;
+      if (warp < 4) {
+        // ---------------- epilogue warps ----------------
+        const float *bsrc = p.w[st.wset].b;
+        for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
+        for (int t = blockIdx.x; t < T; t += gridDim.x) {
+          const uint32_t acc = pipe.ti & 1u;
+          const uint32_t tacc = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * 256u;
+          const int row_tile = t / st.n_col_tiles, col_tile = t % st.n_col_tiles;
+          const uint32_t par = (pipe.ti >> 1) & 1u;
+          switch (st.cell) {
+            case ED_CELL_TREELSTM_LEAF:
+              umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case ED_CELL_TREELSTM_INTERNAL:
+              umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case ED_CELL_TREEGRU_LEAF:
+              umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case ED_CELL_TREEGRU_INTERNAL:
+              umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case ED_CELL_TREEFC_INTERNAL:
+              umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case ED_CELL_LSTM:
+              umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            default:
+              umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+          }
+          ED_TRACE(p, s, 5, tid == 0 && t == (int)blockIdx.x);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // h rows are read by TMA in later steps
+          tc_fence_before();
+          mbar_arrive(tempty + acc);
+          ED_TRACE(p, s, 6, tid == 0 && t == (int)blockIdx.x);
+          ++pipe.ti;
+        }
+      } else if (warp == 4) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc = idesc_bf16(ncols);
+        for (int t = blockIdx.x; t < T; t += gridDim.x) {
+          const uint32_t acc = pipe.ti & 1u;
+          if (lane == 0) {
+            mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
+            tc_fence_after();
+            const uint32_t d = tmem_base + acc * 256u;
+            for (int kc = 0; kc < kc_total; ++kc) {
+              const uint32_t stg = pipe.it % kStages;
+              mbar_wait(full + stg, (pipe.it / kStages) & 1u);
+              tc_fence_after();
+              ED_TRACE(p, s, 3, kc == 0 && t == (int)blockIdx.x);
+              ED_TRACE(p, s, 8 + (kc & 15), t == (int)blockIdx.x);
+              const uint32_t a_addr = smem_u32(stages + stg * kStageBytes);
+              const uint32_t b_addr = a_addr + kAStage;
+              const uint64_t ad = sw128_desc(a_addr), bd = sw128_desc(b_addr);
+#pragma unroll
+              for (int k = 0; k < kChunkK / 16; ++k)
+                tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc > 0 || k > 0) ? 1u : 0u);
+              tc_commit(empty + stg);
+              ++pipe.it;
+            }
+            tc_commit(tfull + acc);
+            ED_TRACE(p, s, 4, t == (int)blockIdx.x);
+          }
+          ++pipe.ti;
+        }
+        pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
+      } else if (warp == 5) {
+        // ---------------- weight (B) loader ----------------
+        const uint8_t *Wp = static_cast<const uint8_t *>(p.w[st.wset].W);
+        const size_t ntot = static_cast<size_t>(st.gates) * h;
+        for (int t = blockIdx.x; t < T; t += gridDim.x) {
+          const int col_tile = t % st.n_col_tiles;
+          if (lane == 0) {
+            for (int kc = 0; kc < kc_total; ++kc) {
+              const uint32_t stg = pipe.it % kStages;
+              mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+              ED_TRACE(p, s, 24 + (kc & 15), t == (int)blockIdx.x);
+              mbar_arrive_tx(full + stg, static_cast<uint32_t>(ncols) * 128u);
+              const uint8_t *src = Wp + ((static_cast<size_t>(kc) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
+              bulk_g2s(stages + stg * kStageBytes + kAStage, src, static_cast<uint32_t>(ncols) * 128u, full + stg);
+              ++pipe.it;
+            }
+          }
+        }
+        pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
+      } else {
+        // ---------------- operand (A) loaders: warps 6-7 (64 threads) ----------------
+        // A CONTIG operand (layout plan made its rows adjacent and aligned) is one TMA 128-row box.
+        // A gathered operand is fetched with 16 B cp.async per (row, chunk) from a per-tile table of
+        // row pointers (H rows or embedding rows); measured on B200 this beats TMA tile::gather4 for
+        // 128 B rows.  Each stage is released to the MMA with a lag of kLag stages.
+        const int lt = tid - 192;
+        const int nseg = cell_segments_dev(st.cell);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // H rows of earlier steps: generic -> async proxy
+        for (int t = blockIdx.x; t < T; t += gridDim.x) {
+          const int row_tile = t / st.n_col_tiles;
+          const void **tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
+          ++tab_tile;
+          for (int r = lt; r < kTileM; r += 64) {
+            const int i = row_tile * kTileM + r;
+            const int iv = i < st.m ? i : (st.m - 1);  // rows past m repeat the last valid row
+#pragma unroll
+            for (int sg = 0; sg < 2; ++sg)
+              tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv))
+                                          : p.H;
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          if (lt == 0) ED_TRACE(p, s, 1, t == (int)blockIdx.x);
+          const int nrows = min(kTileM, st.m - row_tile * kTileM);
+          for (int kc = 0; kc < kc_total; ++kc) {
+            const uint32_t stg = pipe.it % kStages;
+            mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+            const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
+            uint8_t *a_dst = stages + stg * kStageBytes;
+            int cbase = -1;
+            if (segment_contig(st, seg, &cbase)) {
+              if (lt == 0) {
+                mbar_arrive_tx(full + stg, kAStage);
+                tma_row_box(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
+              }
+            } else {
+              if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
+              const uint32_t a_base = smem_u32(a_dst);
+              for (int c = lt; c < nrows * 8; c += 64) {  // rows past m are not loaded
+                const int r = c >> 3, ch = c & 7;
+                const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
+                cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
+              }
+            }
+            cp_async_commit();
+            if (++cp_pending == kLag) {
+              cp_async_wait<kLag - 1>();
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(full + (pipe.it + 1 - kLag) % kStages);
+              --cp_pending;
+            }
+            ++pipe.it;
+          }
+          if (lt == 0) ED_TRACE(p, s, 2, t == (int)blockIdx.x);
+        }
+        // drain: release every stage still pending in this step
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        __syncwarp();
+        for (; cp_pending > 0; --cp_pending)
+          if (lane == 0) mbar_arrive(full + (pipe.it - cp_pending) % kStages);
+      }
+    }
+    ED_TRACE(p, s, 7, tid == 0);
+    grid_sync(p.bar, p.launch_id, epoch);
+    if (blockIdx.x == 0 && tid == 0) p.ts[s + 1] = globaltimer();
+  }
+  collect_roots<__nv_bfloat16>(p);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
+// ------------------------------------------------------------------------------------------------
+// weight packing
+// ------------------------------------------------------------------------------------------------
+// bf16 tensor-core layout of a logical [G*h, K] matrix: [K/64][G*h][64] bf16, packed row p holds
+// logical row g*h + j with p = (j/16)*(G*16) + g*16 + j%16 (gate-interleaved in 16-unit groups),
+// and each 8-row x 128 B atom is 128B-swizzled (16 B chunk c of row r stored at c ^ (r & 7)).
+__global__ void pack_umma_kernel(const float *src, __nv_bfloat16 *dst, int G, int h, int K) {
+  const long N = static_cast<long>(G) * h;
+  const long total = N * K;
+  for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long pr = q / K;       // packed row
+    const int k = static_cast<int>(q % K);
+    const long grp = pr / (G * 16);
+    const int within = static_cast<int>(pr % (G * 16));
+    const int g = within / 16;
+    const long j = grp * 16 + within % 16;
+    const float v = src[(static_cast<long>(g) * h + j) * K + k];
+    const int kc = k / 64, kk = k % 64;
+    const int ch = kk / 8, e = kk % 8;
+    const long byte = (static_cast<long>(kc) * N + pr) * 128 + ((ch ^ static_cast<int>(pr & 7)) * 16) + e * 2;
+    dst[byte / 2] = __float2bfloat16_rn(v);
+  }
+}
+
+// SIMT layout: Wt[k][n] = W[n][k] (element type T).
+template <typename T>
+__global__ void pack_transpose_kernel(const float *src, T *dst, long N, long K) {
+  const long total = N * K;
+  for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long k = q / N, n = q % N;
+    dst[q] = from_f<T>(src[n * K + k]);
+  }
+}
+
+__global__ void copy_f32_kernel(const float *src, float *dst, long n) {
+  for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<long>(gridDim.x) * blockDim.x)
+    dst[q] = src[q];
+}
+
+static bool umma_cell_host(int cell) {
+  return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
+         cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
+         cell == ED_CELL_LATTICE_CHAR;
+}
+
+// Logical shape of a cell's matrices (rows, cols).
+static void logical_shape(int cell, int h, int out_dim, int which, long *rows, long *cols) {
+  if (cell == ED_CELL_LINEAR_OUT) { *rows = out_dim; *cols = h; return; }
+  if (which == 1) {
+    if (cell == ED_CELL_TAGGER) { *rows = out_dim; *cols = h; return; }
+    *rows = h; *cols = 2 * h; return;   // lattice link gate W_l, MV-RNN W_M
+  }
+  *rows = static_cast<long>(cell_gates(cell)) * h;
+  *cols = static_cast<long>(cell_segments(cell)) * h;
+}
+
+int64_t packed_bytes(int cell, int hidden, int out_dim, int dtype, int which) {
+  long rows = 0, cols = 0;
+  logical_shape(cell, hidden, out_dim, which, &rows, &cols);
+  if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) return rows * cols * 4;
+  return rows * cols * (dtype == ED_BF16 ? 2 : 4);
+}
+
+int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const float *src, void *dst,
+                void *stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long rows = 0, cols = 0;
+  logical_shape(cell, hidden, out_dim, which, &rows, &cols);
+  const int threads = 256;
+  const long total = rows * cols;
+  const int blocks = static_cast<int>((total + threads - 1) / threads < 4096 ? (total + threads - 1) / threads : 4096);
+  if (total == 0) return 0;
+  if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) {
+    copy_f32_kernel<<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), total);
+  } else if (dtype == ED_BF16 && which == 0 && umma_cell_host(cell)) {
+    if (hidden % 64 != 0) return static_cast<int>(cudaErrorInvalidValue);
+    pack_umma_kernel<<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), cell_gates(cell), hidden,
+                                                static_cast<int>(cols));
+  } else if (dtype == ED_BF16) {
+    pack_transpose_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), rows, cols);
+  } else {
+    pack_transpose_kernel<float><<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), rows, cols);
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------------------------------------
+// launch
+// ------------------------------------------------------------------------------------------------
+int device_check(int *sm_count, int *major, int *minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return static_cast<int>(e);
+}
+
+int persistent_grid(int dtype, int *grid) {
+  int sms = 0, major = 0, minor = 0;
+  int e = device_check(&sms, &major, &minor);
+  if (e) return e;
+  int per_sm = 0;
+  if (dtype == ED_BF16) {
+    cudaError_t ce = cudaFuncSetAttribute(ed_persistent_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (ce != cudaSuccess) return static_cast<int>(ce);
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ed_persistent_bf16, kThreads, kSmemBytes);
+    if (ce != cudaSuccess) return static_cast<int>(ce);
+    if (per_sm > 1) per_sm = 1;  // TMEM: one 512-column allocation per SM
+  } else {
+    cudaError_t ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ed_persistent_f32, kThreads, 0);
+    if (ce != cudaSuccess) return static_cast<int>(ce);
+    if (per_sm > 2) per_sm = 2;
+  }
+  *grid = sms * (per_sm > 0 ? per_sm : 1);
+  return 0;
+}
+
+int launch_persistent(const KParams &p, int dtype, int grid, void *stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(p.bar, 0, 256, s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  void *args[] = {const_cast<KParams *>(&p)};
+  if (dtype == ED_BF16) {
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_bf16), dim3(grid), dim3(kThreads), args,
+                                    kSmemBytes, s);
+  } else {
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_f32), dim3(grid), dim3(kThreads), args, 0,
+                                    s);
+  }
+  return static_cast<int>(e);
+}
+
+}  // namespace ed

@@ -1,0 +1,319 @@
+"""Thin ctypes binding of libedbatch.so (include/ed_batch.h) — argument marshalling only.
+
+Every step of the hot path runs in the library: ed_plan (host C++ scheduler + layout planner)
+and ed_execute (one persistent sm_100a kernel).  PyTorch supplies device memory and streams.
+There is no fallback: if libedbatch.so is missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libedbatch.so")
+
+ED_OK = 0
+ED_ZERO_INPUT = -(2 ** 31)
+ED_FP32, ED_BF16 = 0, 1
+ED_ENC_SORT, ED_ENC_BASE = 0, 1
+ED_LAYOUT_SCHEDULE_ORDER, ED_LAYOUT_PQ = 0, 1
+STATUS = {0: "ED_OK", -1: "ED_E_INVALID_ARG", -2: "ED_E_CYCLE", -3: "ED_E_DANGLING", -4: "ED_E_DUP_ID",
+          -5: "ED_E_TYPE", -6: "ED_E_ARITY", -7: "ED_E_FSM", -8: "ED_E_CUDA", -9: "ED_E_UNSUPPORTED",
+          -10: "ED_E_WORKSPACE", -11: "ED_E_OOM"}
+CELL = {"treelstm_leaf": 1, "treelstm_internal": 2, "linear_out": 3, "treegru_leaf": 4,
+        "treegru_internal": 5, "treefc_internal": 6, "lstm": 7, "tagger": 8, "mvrnn_internal": 9,
+        "lattice_char": 10, "lattice_word": 11}
+DTYPE = {"fp32": ED_FP32, "bf16": ED_BF16}
+
+_p = ctypes.POINTER
+_i32p = _p(ctypes.c_int32)
+
+
+class ed_op_type_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("cell_kind", "num_slots", "variadic", "has_ext", "weight_set", "hidden", "out_dim", "dtype")]
+
+
+class ed_graph_t(ctypes.Structure):
+    _fields_ = [("num_nodes", ctypes.c_int32), ("type", _i32p), ("in_off", _i32p), ("in_idx", _i32p),
+                ("ext", _i32p), ("root", ctypes.c_int32)]
+
+
+class ed_fsm_entry_t(ctypes.Structure):
+    _fields_ = [("key_len", ctypes.c_int32), ("key", _i32p), ("action", ctypes.c_int32)]
+
+
+class ed_fsm_t(ctypes.Structure):
+    _fields_ = [("encoder", ctypes.c_int32), ("num_entries", ctypes.c_int32), ("entries", _p(ed_fsm_entry_t)),
+                ("fallback", ctypes.c_int32)]
+
+
+class ed_plan_opts_t(ctypes.Structure):
+    _fields_ = [("layout", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+_INFO_I64 = ("num_nodes", "num_instances", "num_batches", "lower_bound", "num_rows", "hidden", "dtype",
+             "workspace_bytes", "contig_operands", "gather_operands", "copy_bytes", "copy_kernels", "off_h",
+             "off_c", "off_y", "y_cols", "off_x", "off_ts")
+
+
+class ed_plan_info_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in _INFO_I64] + [
+        ("plan_us", ctypes.c_double), ("schedule_us", ctypes.c_double), ("layout_us", ctypes.c_double)]
+
+
+class ed_weight_set_t(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_void_p), ("b", ctypes.c_void_p), ("W2", ctypes.c_void_p), ("b2", ctypes.c_void_p),
+                ("emb", ctypes.c_void_p), ("emb2", ctypes.c_void_p), ("mat", ctypes.c_void_p),
+                ("emb_rows", ctypes.c_int32), ("emb2_rows", ctypes.c_int32)]
+
+
+class ed_weights_t(ctypes.Structure):
+    _fields_ = [("num_sets", ctypes.c_int32), ("sets", _p(ed_weight_set_t))]
+
+
+class ed_io_t(ctypes.Structure):
+    _fields_ = [("out_root", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
+
+
+class EdError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2302_03851_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.ed_plan.argtypes = [_p(ed_graph_t), ctypes.c_int32, _p(ed_op_type_t), ctypes.c_int32, _p(ed_fsm_t),
+                            _p(ed_plan_opts_t), _p(ctypes.c_void_p)]
+    lib.ed_plan_info.argtypes = [ctypes.c_void_p, _p(ed_plan_info_t)]
+    lib.ed_plan_get_schedule.argtypes = [ctypes.c_void_p, _i32p, _i32p, _i32p]
+    lib.ed_plan_get_layout.argtypes = [ctypes.c_void_p, _i32p]
+    lib.ed_plan_get_slot_modes.argtypes = [ctypes.c_void_p, _i32p]
+    lib.ed_plan_destroy.argtypes = [ctypes.c_void_p]
+    lib.ed_plan_destroy.restype = None
+    lib.ed_packed_bytes.argtypes = [ctypes.c_int32] * 5
+    lib.ed_packed_bytes.restype = ctypes.c_int64
+    lib.ed_pack_weights.argtypes = [ctypes.c_int32] * 5 + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.ed_execute.argtypes = [ctypes.c_void_p, _p(ed_weights_t), _p(ed_io_t), ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_void_p]
+    lib.ed_execute_launch_count.argtypes = [ctypes.c_void_p]
+    lib.ed_last_error.restype = ctypes.c_char_p
+    lib.ed_version.restype = ctypes.c_char_p
+    for f in ("ed_plan", "ed_plan_info", "ed_plan_get_schedule", "ed_plan_get_layout", "ed_plan_get_slot_modes",
+              "ed_pack_weights", "ed_execute", "ed_execute_launch_count"):
+        getattr(lib, f).restype = ctypes.c_int32
+    return lib
+
+
+LIB = _load()
+
+
+def _check(code: int):
+    if code != ED_OK:
+        raise EdError(code, LIB.ed_last_error().decode())
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_i32p)
+
+
+def fsm_from_priority(priority: Sequence[int], num_types: int) -> List[Tuple[Tuple[int, ...], int]]:
+    """FSM table as (E_sort key, action) entries for every key: the highest-priority type present."""
+    import itertools
+    rank = {t: i for i, t in enumerate(priority)}
+    out = []
+    for k in range(1, num_types + 1):
+        for key in itertools.permutations(range(num_types), k):
+            out.append((key, min(key, key=lambda t: rank.get(t, len(rank) + t))))
+    return out
+
+
+class Plan:
+    """Owning wrapper of an ed_plan_t handle."""
+
+    def __init__(self, handle: ctypes.c_void_p, num_types: int):
+        self.handle = handle
+        self.num_types = num_types
+        info = ed_plan_info_t()
+        _check(LIB.ed_plan_info(handle, ctypes.byref(info)))
+        self.info = {n: getattr(info, n) for n, _ in ed_plan_info_t._fields_}
+
+    def __del__(self):
+        if getattr(self, "handle", None) and LIB is not None:
+            LIB.ed_plan_destroy(self.handle)
+            self.handle = None
+
+    def schedule(self) -> List[Tuple[int, List[int]]]:
+        nb, V = self.info["num_batches"], self.info["num_nodes"]
+        bt = np.zeros(nb, np.int32); bo = np.zeros(nb + 1, np.int32); mem = np.zeros(max(V, 1), np.int32)
+        _check(LIB.ed_plan_get_schedule(self.handle, _ptr(bt), _ptr(bo), _ptr(mem)))
+        return [(int(bt[b]), [int(x) for x in mem[bo[b]:bo[b + 1]]]) for b in range(nb)]
+
+    def layout(self) -> np.ndarray:
+        row = np.zeros(max(self.info["num_nodes"], 1), np.int32)
+        _check(LIB.ed_plan_get_layout(self.handle, _ptr(row)))
+        return row[:self.info["num_nodes"]]
+
+    def slot_modes(self) -> np.ndarray:
+        m = np.zeros(max(2 * self.info["num_batches"], 1), np.int32)
+        _check(LIB.ed_plan_get_slot_modes(self.handle, _ptr(m)))
+        return m[:2 * self.info["num_batches"]].reshape(-1, 2)
+
+    @property
+    def launches(self) -> int:
+        return LIB.ed_execute_launch_count(self.handle)
+
+
+def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: int = ED_ENC_SORT,
+            layout: int = ED_LAYOUT_SCHEDULE_ORDER) -> Plan:
+    """graphs: objects with numpy fields type/in_off/in_idx/ext and int root (workloads.Graph);
+    types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype."""
+    keep = []
+    garr = (ed_graph_t * max(len(graphs), 1))()
+    for k, g in enumerate(graphs):
+        arrs = [_i32(g.type), _i32(g.in_off), _i32(g.in_idx) if len(g.in_idx) else _i32([0]), _i32(g.ext)]
+        keep.append(arrs)
+        garr[k] = ed_graph_t(int(len(g.type)), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), int(g.root))
+    tarr = (ed_op_type_t * len(types))()
+    for k, t in enumerate(types):
+        tarr[k] = ed_op_type_t(CELL[t.kind], t.num_slots, t.variadic, t.has_ext, t.weight_set, t.hidden,
+                               t.out_dim, DTYPE[t.dtype])
+    earr = (ed_fsm_entry_t * max(len(fsm), 1))()
+    for k, (key, act) in enumerate(fsm):
+        ka = _i32(list(key))
+        keep.append(ka)
+        earr[k] = ed_fsm_entry_t(len(ka), _ptr(ka), int(act))
+    f = ed_fsm_t(encoder, len(fsm), earr, 0)
+    opts = ed_plan_opts_t(layout, (ctypes.c_int32 * 7)())
+    h = ctypes.c_void_p()
+    _check(LIB.ed_plan(garr, len(graphs), tarr, len(types), ctypes.byref(f), ctypes.byref(opts), ctypes.byref(h)))
+    return Plan(h, len(types))
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ed_packed_bytes(kind: str, hidden: int, out_dim: int, dtype: str, which: int) -> int:
+    return int(LIB.ed_packed_bytes(CELL[kind], hidden, out_dim, DTYPE[dtype], which))
+
+
+def ed_pack_weights(kind: str, hidden: int, out_dim: int, dtype: str, which: int, logical: torch.Tensor,
+                    stream=None) -> torch.Tensor:
+    logical = logical.to(torch.float32).contiguous()
+    nbytes = ed_packed_bytes(kind, hidden, out_dim, dtype, which)
+    out = torch.empty(nbytes, dtype=torch.uint8, device=logical.device)
+    _check(LIB.ed_pack_weights(CELL[kind], hidden, out_dim, DTYPE[dtype], which,
+                               ctypes.c_void_p(logical.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                               _stream_handle(stream)))
+    return out
+
+
+_SECOND = {"tagger": ("W2", "b2"), "lattice_word": ("Wl", "bl"), "mvrnn_internal": ("WM", None)}
+
+
+class DeviceWeights:
+    """Weights of a workload on the device, packed by ed_pack_weights (marshalling only)."""
+
+    def __init__(self, types, params: List[Dict[str, np.ndarray]], device="cuda", stream=None):
+        self.tensors: List[Dict[str, torch.Tensor]] = []
+        tdt = {"bf16": torch.bfloat16, "fp32": torch.float32}
+        kinds = {}
+        for t in types:
+            kinds.setdefault(t.weight_set, t)
+        for ws, p in enumerate(params):
+            t = kinds.get(ws)
+            d: Dict[str, torch.Tensor] = {}
+            if t is not None:
+                dt = tdt[t.dtype]
+                d["W"] = ed_pack_weights(t.kind, t.hidden, t.out_dim, t.dtype, 0,
+                                         torch.from_numpy(p["W"]).to(device), stream)
+                d["b"] = torch.from_numpy(np.asarray(p["b"], np.float32)).to(device)
+                if t.kind in _SECOND:
+                    wk, bk = _SECOND[t.kind]
+                    d["W2"] = ed_pack_weights(t.kind, t.hidden, t.out_dim, t.dtype, 1,
+                                              torch.from_numpy(p[wk]).to(device), stream)
+                    if bk:
+                        d["b2"] = torch.from_numpy(np.asarray(p[bk], np.float32)).to(device)
+                for k in ("emb", "emb2", "mat"):
+                    if k in p:
+                        d[k] = torch.from_numpy(np.asarray(p[k], np.float32)).to(device=device, dtype=dt).contiguous()
+            self.tensors.append(d)
+        arr = (ed_weight_set_t * len(self.tensors))()
+        for k, d in enumerate(self.tensors):
+            g = lambda n: ctypes.c_void_p(d[n].data_ptr()) if n in d else None
+            arr[k] = ed_weight_set_t(g("W"), g("b"), g("W2"), g("b2"), g("emb"), g("emb2"), g("mat"),
+                                     int(d["emb"].shape[0]) if "emb" in d else 0,
+                                     int(d["emb2"].shape[0]) if "emb2" in d else 0)
+        self._arr = arr
+        self.struct = ed_weights_t(len(self.tensors), arr)
+
+
+class Workspace:
+    """Caller-owned device workspace (1024-aligned) with typed views of the row buffers."""
+
+    def __init__(self, plan: Plan, device="cuda"):
+        nbytes = int(plan.info["workspace_bytes"])
+        self.raw = torch.zeros(nbytes + 1024, dtype=torch.uint8, device=device)
+        off = (-self.raw.data_ptr()) % 1024
+        self.buf = self.raw[off:off + nbytes]
+        self.nbytes = nbytes
+        self.plan_info = plan.info
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def _view(self, off: int, count: int, dtype) -> torch.Tensor:
+        es = torch.tensor([], dtype=dtype).element_size()
+        return self.buf[off:off + count * es].view(dtype)
+
+    def H(self) -> torch.Tensor:
+        i = self.plan_info
+        dt = torch.bfloat16 if i["dtype"] == ED_BF16 else torch.float32
+        return self._view(i["off_h"], i["num_rows"] * i["hidden"], dt).view(i["num_rows"], i["hidden"])
+
+    def C(self) -> torch.Tensor:
+        i = self.plan_info
+        return self._view(i["off_c"], i["num_rows"] * i["hidden"], torch.float32).view(i["num_rows"], i["hidden"])
+
+    def Y(self) -> torch.Tensor:
+        i = self.plan_info
+        return self._view(i["off_y"], i["num_rows"] * i["y_cols"], torch.float32).view(i["num_rows"], i["y_cols"])
+
+    def X(self) -> Optional[torch.Tensor]:
+        i = self.plan_info
+        if i["off_x"] < 0:
+            return None
+        return self._view(i["off_x"], i["num_rows"] * i["hidden"], torch.float32).view(i["num_rows"], i["hidden"])
+
+    def step_times_ns(self) -> np.ndarray:
+        i = self.plan_info
+        ts = self._view(i["off_ts"], i["num_batches"] + 1, torch.int64).cpu().numpy()
+        return np.diff(ts)
+
+
+def ed_execute(plan: Plan, weights: DeviceWeights, workspace: Workspace, out_root: Optional[torch.Tensor] = None,
+               stream=None, trace: Optional[torch.Tensor] = None) -> None:
+    io = ed_io_t(ctypes.c_void_p(out_root.data_ptr()) if out_root is not None else None,
+                 ctypes.c_void_p(trace.data_ptr()) if trace is not None else None)
+    _check(LIB.ed_execute(plan.handle, ctypes.byref(weights.struct), ctypes.byref(io),
+                          ctypes.c_void_p(workspace.ptr), workspace.nbytes, _stream_handle(stream)))
+
+
+def version() -> str:
+    return LIB.ed_version().decode()
