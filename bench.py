@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — ED-Batch hot path (arXiv 2302.03851) on B200: instances/s of one full batched
+forward pass (every batch of the FSM schedule) over a minibatch of synthetic instance graphs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
+
+A "step" is one ed_execute (one persistent kernel) over the minibatch (BASELINE cfg3: 256
+TreeLSTM trees, h = 512, bf16), inputs resident in HBM; L2 (126 MB) is flushed between timed
+steps by a 256 MB write.  Multi-GPU: instances are sharded, every rank runs its own minibatch of
+the same size (weak scaling) with no data-path collective; time = max over ranks.
+Prints ONE JSON line (rank 0).  DESIGN.md §7 documents every field.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "instances/sec TreeLSTM h=512 (BASELINE cfg3: 256 random trees, bf16) per step, whole job"
+CONFIGS = {
+    "cfg3": "cfg3 TreeLSTM h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16, FSM L>I>O",
+    "cfg3_gru": "cfg3 TreeGRU h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
+    "cfg1": "cfg1 TreeLSTM h=32, 8 random trees (leaves U[2,16]), fp32",
+}
+
+
+def make_workload(name: str, rank: int):
+    if rank == 0:
+        return W.config(name)
+    if name in ("cfg3", "cfg3_gru"):
+        return W.treelstm(256, (5, 40), 512, "bf16", 3 + 100 * rank, cell="treegru" if name == "cfg3_gru" else "treelstm")
+    if name == "cfg1":
+        return W.treelstm(8, (2, 16), 32, "fp32", 1 + 100 * rank)
+    raise KeyError(name)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), float(d["hbm_gbs"]), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# --- algorithmic work per batch -----------------------------------
+def step_work(kind: str, m: int, h: int, C: int, elt: int):
+    """(flops, hbm bytes) of one batch of m ops, weights excluded."""
+    if kind == "treelstm_leaf":
+        return 2 * m * h * 3 * h, m * (elt * h + 4 + elt * h + 4 * h)
+    if kind == "treelstm_internal":
+        return 2 * m * 2 * h * 5 * h, m * (2 * elt * h + 2 * 4 * h + elt * h + 4 * h)
+    if kind == "linear_out":
+        return 2 * m * h * C, m * (elt * h + 4 * C)
+    if kind == "treegru_leaf":
+        return 2 * m * h * 2 * h, m * (elt * h + 4 + elt * h)
+    if kind == "treegru_internal":
+        return 2 * m * (2 * h * 3 * h + 2 * h * h), m * (2 * elt * h + elt * h)
+    if kind == "treefc_internal":
+        return 2 * m * 2 * h * h, m * (2 * elt * h + elt * h)
+    if kind == "lstm":
+        return 2 * m * 2 * h * 4 * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h)
+    raise KeyError(kind)
+
+
+def weight_bytes(kind: str, h: int, C: int, elt: int) -> int:
+    g = {"treelstm_leaf": (3, 1), "treelstm_internal": (5, 2), "treegru_leaf": (2, 1), "treegru_internal": (5, 2),
+         "treefc_internal": (1, 2), "lstm": (4, 2)}
+    if kind == "linear_out":
+        return 4 * C * h
+    G, S = g[kind]
+    return elt * G * h * S * h + 4 * G * h
+
+
+def plan_roofline(wl, plan, P_tflops, BW_gbs):
+    """Per-batch roofline t_roof = max(F / P, B / BW); weights charged once per pass (first use)."""
+    elt = 2 if wl.dtype == "bf16" else 4
+    seen = set()
+    F_tot = B_tot = 0
+    troof = []
+    for t, mem in plan.schedule():
+        ot = wl.types[t]
+        F, B = step_work(ot.kind, len(mem), wl.hidden, ot.out_dim, elt)
+        if ot.weight_set not in seen:
+            seen.add(ot.weight_set)
+            B += weight_bytes(ot.kind, wl.hidden, ot.out_dim, elt)
+        F_tot += F
+        B_tot += B
+        troof.append(max(F / (P_tflops * 1e12), B / (BW_gbs * 1e9)))
+    return F_tot, B_tot, troof
+
+
+# --- clocks ---------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self, ngpu: int):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= ngpu:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --- CPU oracle baseline (bounded sample) -------------------------------------------------------
+def cpu_oracle_rate(wl, seconds: float, max_instances: int = 256):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle.evaluate import evaluate_recursive
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        limiter = None
+    n = 0
+    t0 = time.perf_counter()
+    while n < max_instances and time.perf_counter() - t0 < seconds:
+        evaluate_recursive(wl, [n % len(wl.graphs)])
+        n += 1
+    dt = time.perf_counter() - t0
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    return n / dt, n, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle (plain per-node topological evaluation) on host cores,
+    each step a bounded sample of the same workload; rank 0 only."""
+    if rank != 0:
+        return
+    wl = make_workload(args.config, 0)
+    sample = args.ref_sample
+    from oracle.evaluate import evaluate_recursive
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    times = []
+    for s in range(args.warmup + args.steps):
+        idx = [(s * sample + k) % len(wl.graphs) for k in range(sample)]
+        t0 = time.perf_counter()
+        evaluate_recursive(wl, idx)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    v = sample / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config], "sample_instances_per_step": sample},
+            "cpu_baseline": {"value": v, "unit": "instances/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{sample} instances per step of the {args.config} minibatch, fp64 per-node "
+                                       "recursive oracle (oracle/evaluate.py), 1 BLAS thread"},
+            "e2e": {"value": v, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layout", default="schedule", choices=["schedule", "pq"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-sample", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2302_03851_b200 import edbatch as E
+
+    wl = make_workload(args.config, rank)
+    layout = E.ED_LAYOUT_PQ if args.layout == "pq" else E.ED_LAYOUT_SCHEDULE_ORDER
+    fsm = E.fsm_from_priority(wl.priority, len(wl.types))
+    plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout)
+    weights = E.DeviceWeights(wl.types, wl.params)
+    ws = E.Workspace(plan)
+    tdt = torch.bfloat16 if wl.dtype == "bf16" else torch.float32
+    out = torch.zeros(len(wl.graphs), wl.hidden, dtype=tdt, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 256 MB > L2
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        E.ed_execute(plan, weights, ws, out)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    step_ns = []
+    for k in range(args.steps):
+        flush.zero_()                          # untimed: evict L2 between timed steps
+        evs[k][0].record(stream)
+        E.ed_execute(plan, weights, ws, out)
+        evs[k][1].record(stream)
+        if k == args.steps - 1:
+            pass
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clock_rec = clocks.stop(max(world, 1)) if rank == 0 else None
+    times = [a.elapsed_time(b) for a, b in evs]
+    ms_local = sum(times) / len(times)
+    step_ns = ws.step_times_ns()               # in-kernel %globaltimer, last timed execute
+    ms = ms_local
+    if dist:
+        t = torch.tensor([ms_local], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_inst_total = len(wl.graphs) * world
+    value = n_inst_total / (ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers: ed_plan + upload + execute + readback
+    host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    e2e_times = []
+    h2d = d2h = 0
+    for k in range(args.e2e_steps + 2):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        p2 = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout)   # host scheduling + layout
+        ws.plan_info = p2.info
+        E.ed_execute(p2, weights, ws, out)                         # uploads the step table (H2D)
+        host_out.copy_(out, non_blocking=True)                     # D2H of the step's result
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k >= 2:
+            e2e_times.append(a.elapsed_time(b))
+        h2d, d2h = p2.upload_bytes, out.numel() * out.element_size()
+        del p2
+    ws.plan_info = plan.info
+    e2e_ms = sum(e2e_times) / len(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank == 0:
+        P, P_sus, BW, src = peaks()
+        F_tot, B_tot, troof = plan_roofline(wl, plan, P, BW)
+        achieved = F_tot / (ms_local / 1e3) / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_summary.json")
+        if os.path.exists(prof):
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        meas = [x / 1e9 for x in step_ns]
+        per_step = {"sum_t_roof_us": 1e6 * sum(troof), "sum_t_meas_us": 1e6 * sum(meas),
+                    "frac": (sum(troof) / sum(meas)) if sum(meas) > 0 else None,
+                    "steps": [{"type": wl.types[t].name, "m": len(mem), "t_roof_us": round(1e6 * r, 3),
+                               "t_meas_us": round(1e6 * s_, 3)}
+                              for (t, mem), r, s_ in zip(plan.schedule(), troof, meas)]}
+        cpu_rate, cpu_n, cpu_dt = cpu_oracle_rate(wl, args.cpu_seconds) if world == 1 or rank == 0 else (None, 0, 0)
+        line = {
+            "metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded parse-like trees, random-init weights)",
+            "config": {"workload": CONFIGS[args.config], "instances_per_gpu": len(wl.graphs),
+                       "nodes_per_gpu": wl.num_nodes, "batches": plan.info["num_batches"],
+                       "lower_bound": plan.info["lower_bound"], "layout": args.layout,
+                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world}"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
+                         "frac": achieved / P, "traffic": traffic,
+                         "kernel": "ed_persistent_bf16" if wl.dtype == "bf16" else "ed_persistent_f32",
+                         "algorithmic_flops_per_launch": F_tot, "algorithmic_bytes_per_launch": B_tot,
+                         "peak_source": f"{src} bf16_tflops (burst; kernel timed alone)"},
+            "per_step_roofline": per_step,
+            "cpu_baseline": {"value": cpu_rate, "unit": "instances/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{cpu_n} instances of the {args.config} minibatch in {cpu_dt:.1f} s, fp64 "
+                                       "per-node recursive oracle, 1 BLAS thread"},
+            "e2e": {"value": n_inst_total / (e2e_ms / 1e3), "unit": "instances/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "includes": "ed_plan (host Alg. 1 + layout) + step-table H2D + ed_execute + root D2H"},
+            "gpu_launches": args.steps * plan.launches,
+            "clocks": clock_rec,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -213,6 +213,10 @@ ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, 
 ed_status_t ed_execute(ed_plan_t *plan, const ed_weights_t *weights, const ed_io_t *io, void *workspace,
                        size_t workspace_bytes, void *stream);
 
+/* Bytes of the plan's static part (step table, index arrays) that the first ed_execute on a
+ * workspace uploads host->device (through a reused pinned staging buffer). */
+int64_t ed_plan_upload_bytes(const ed_plan_t *plan);
+
 /* Number of kernels ed_execute launches (for launch accounting). */
 int32_t ed_execute_launch_count(const ed_plan_t *plan);
 

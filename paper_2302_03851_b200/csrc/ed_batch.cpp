@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -61,6 +62,59 @@ double now_us() {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Pinned staging buffer for the async H2D upload of a plan's static part (step table, index
+// arrays).  Reused across plans: before it is overwritten the previous copy must have completed
+// (an event recorded after it), so a new minibatch plan needs no cudaMallocHost.
+struct Staging {
+  std::mutex mu;
+  void *buf = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+};
+Staging &staging() {
+  static Staging s;
+  return s;
+}
+
+cudaError_t upload_async(void *dst, const void *src, size_t n, cudaStream_t s) {
+  Staging &st = staging();
+  std::lock_guard<std::mutex> lk(st.mu);
+  cudaError_t e = cudaSuccess;
+  if (st.pending) {
+    e = cudaEventSynchronize(st.done);
+    if (e != cudaSuccess) return e;
+    st.pending = false;
+  }
+  if (n > st.cap) {
+    if (st.buf) cudaFreeHost(st.buf);
+    st.cap = std::max<size_t>(n, size_t(4) << 20);
+    e = cudaMallocHost(&st.buf, st.cap);
+    if (e != cudaSuccess) { st.buf = nullptr; st.cap = 0; return e; }
+  }
+  if (!st.done) {
+    e = cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  std::memcpy(st.buf, src, n);
+  e = cudaMemcpyAsync(dst, st.buf, n, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  e = cudaEventRecord(st.done, s);
+  st.pending = (e == cudaSuccess);
+  return e;
+}
+
+// Which plan's static part currently sits in which workspace (a workspace can be shared by
+// several plans; the step table is re-uploaded whenever the owner changes).
+struct WsRegistry {
+  std::mutex mu;
+  std::map<const void *, const void *> owner;  // workspace -> plan
+};
+WsRegistry &ws_registry() {
+  static WsRegistry r;
+  return r;
+}
+
 }  // namespace
 
 struct ed_plan_s {
@@ -93,8 +147,6 @@ struct ed_plan_s {
   double plan_us = 0, sched_us = 0, layout_us = 0;
   // upload state
   std::vector<uint8_t> blob;          // [ts zeros | steps | idx | roots]
-  void *pinned = nullptr;
-  const void *uploaded_ws = nullptr;
   int grid = 0;
   uint32_t launches = 0;
 };
@@ -373,7 +425,7 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->off_ts = off; off = align_up(off + 8 * static_cast<size_t>(nb + 1), 256);
   pl->off_steps = off; off = align_up(off + sizeof(ed::DevStep) * nb, 256);
   pl->off_idx = off; off = align_up(off + 4 * pl->idx.size(), 256);
-  pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 256);
+  pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 1024);
   pl->off_h = off; off = align_up(off + elt * rows * h, 1024);
   pl->off_c = off; off = align_up(off + 4 * rows * h, 1024);
   pl->y_cols = 0;
@@ -431,6 +483,7 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
     if (ot.num_slots < 0 || ot.num_slots > 2) { delete pl; return fail(ED_E_TYPE, tag + ": num_slots must be 0..2"); }
     if ((ot.cell_kind == ED_CELL_LINEAR_OUT || ot.cell_kind == ED_CELL_TAGGER) && (ot.out_dim <= 0 || ot.out_dim > 16)) { delete pl; return fail(ED_E_TYPE, tag + ": out_dim must be 1..16"); }
     if (ot.dtype == ED_BF16 && ot.hidden % 64 != 0) { delete pl; return fail(ED_E_TYPE, tag + ": bf16 path needs hidden % 64 == 0"); }
+    if (!ed::cell_implemented(ot.cell_kind)) { delete pl; return fail(ED_E_UNSUPPORTED, tag + ": cell kind not implemented by this build"); }
   }
   ed_status_t st = validate_and_merge(pl, graphs, num_graphs);
   if (st != ED_OK) { delete pl; return st; }
@@ -456,6 +509,8 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   *out = pl;
   return ED_OK;
 }
+
+int64_t ed_plan_upload_bytes(const ed_plan_t *pl) { return pl ? static_cast<int64_t>(pl->blob.size()) : 0; }
 
 ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
   if (!pl || !o) return fail(ED_E_INVALID_ARG, "null argument");
@@ -506,7 +561,12 @@ ed_status_t ed_plan_get_slot_modes(const ed_plan_t *pl, int32_t *modes) {
 
 void ed_plan_destroy(ed_plan_t *pl) {
   if (!pl) return;
-  if (pl->pinned) cudaFreeHost(pl->pinned);
+  {
+    WsRegistry &reg = ws_registry();
+    std::lock_guard<std::mutex> lk(reg.mu);
+    for (auto it = reg.owner.begin(); it != reg.owner.end();)
+      it = (it->second == pl) ? reg.owner.erase(it) : std::next(it);
+  }
   delete pl;
 }
 
@@ -543,13 +603,15 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   if (major != 10 || minor != 0) return fail(ED_E_UNSUPPORTED, "device is not sm_100 (sm_" + std::to_string(major * 10 + minor) + ")");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t *base = static_cast<uint8_t *>(ws);
-  if (pl->uploaded_ws != ws) {
-    if (!pl->pinned) {
-      cudaError_t ce = cudaMallocHost(&pl->pinned, pl->blob.size() > 0 ? pl->blob.size() : 1);
-      if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(ce));
-      std::memcpy(pl->pinned, pl->blob.data(), pl->blob.size());
-    }
-    cudaError_t ce = cudaMemcpyAsync(base + pl->off_ts, pl->pinned, pl->blob.size(), cudaMemcpyHostToDevice, s);
+  bool need_upload;
+  {
+    WsRegistry &reg = ws_registry();
+    std::lock_guard<std::mutex> lk(reg.mu);
+    auto it = reg.owner.find(ws);
+    need_upload = (it == reg.owner.end() || it->second != pl);
+  }
+  if (need_upload) {
+    cudaError_t ce = upload_async(base + pl->off_ts, pl->blob.data(), pl->blob.size(), s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_bar, 0, pl->off_ts - pl->off_bar, s);  // barrier flags
     if (ce == cudaSuccess) {
       const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
@@ -559,7 +621,9 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
         ce = cudaMemsetAsync(base + pl->off_x + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
     }
     if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
-    pl->uploaded_ws = ws;
+    WsRegistry &reg = ws_registry();
+    std::lock_guard<std::mutex> lk(reg.mu);
+    reg.owner[ws] = pl;
   }
   if (pl->grid == 0) {
     e = ed::persistent_grid(pl->dtype, &pl->grid);

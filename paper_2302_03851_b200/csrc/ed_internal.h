@@ -106,6 +106,20 @@ inline int cell_units(int cell) {
   }
 }
 
+// Cell kinds the device code implements in this build.
+inline bool cell_implemented(int cell) {
+  switch (cell) {
+    case ED_CELL_TREELSTM_LEAF:
+    case ED_CELL_TREELSTM_INTERNAL:
+    case ED_CELL_LINEAR_OUT:
+    case ED_CELL_TREEGRU_LEAF:
+    case ED_CELL_TREEGRU_INTERNAL:
+    case ED_CELL_TREEFC_INTERNAL:
+    case ED_CELL_LSTM: return true;
+    default: return false;
+  }
+}
+
 // K segments (each of width hidden) of the main contraction.
 inline int cell_segments(int cell) {
   switch (cell) {

@@ -106,6 +106,8 @@ def _load() -> ctypes.CDLL:
     lib.ed_execute.argtypes = [ctypes.c_void_p, _p(ed_weights_t), _p(ed_io_t), ctypes.c_void_p, ctypes.c_size_t,
                                ctypes.c_void_p]
     lib.ed_execute_launch_count.argtypes = [ctypes.c_void_p]
+    lib.ed_plan_upload_bytes.argtypes = [ctypes.c_void_p]
+    lib.ed_plan_upload_bytes.restype = ctypes.c_int64
     lib.ed_last_error.restype = ctypes.c_char_p
     lib.ed_version.restype = ctypes.c_char_p
     for f in ("ed_plan", "ed_plan_info", "ed_plan_get_schedule", "ed_plan_get_layout", "ed_plan_get_slot_modes",
@@ -171,6 +173,10 @@ class Plan:
         m = np.zeros(max(2 * self.info["num_batches"], 1), np.int32)
         _check(LIB.ed_plan_get_slot_modes(self.handle, _ptr(m)))
         return m[:2 * self.info["num_batches"]].reshape(-1, 2)
+
+    @property
+    def upload_bytes(self) -> int:
+        return int(LIB.ed_plan_upload_bytes(self.handle))
 
     @property
     def launches(self) -> int:

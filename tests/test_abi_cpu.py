@@ -1,0 +1,208 @@
+"""C-ABI tests that need no GPU: exports, ed_plan schedules/layouts vs the oracle, error codes.
+
+ed_plan is host-only (C++), so the FSM scheduler and the layout are checked here bit-exactly
+against the independent Python oracle (oracle/schedule.py, oracle/layout.py).
+"""
+import re
+import os
+import ctypes
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import layout as OL
+from oracle import schedule as S
+from oracle.graph import Merged, lower_bound_dp
+
+E = pytest.importorskip("paper_2302_03851_b200.edbatch")
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "ed_batch.h")
+
+
+def test_library_exports_every_declared_symbol():
+    src = open(HDR).read()
+    names = set(re.findall(r"^[A-Za-z_][\w \*]*?\b(ed_\w+)\s*\(", src, flags=re.M))
+    assert {"ed_plan", "ed_execute", "ed_pack_weights", "ed_plan_info", "ed_plan_destroy",
+            "ed_last_error"} <= names
+    for n in names:
+        assert hasattr(E.LIB, n), n
+    assert E.version().startswith("ed_batch")
+
+
+def _plan(wl, layout=0, priority=None, encoder=0):
+    pr = wl.priority if priority is None else priority
+    return E.ed_plan(wl.graphs, wl.types, E.fsm_from_priority(pr, len(wl.types)), encoder=encoder, layout=layout)
+
+
+def _oracle_schedule(wl, priority=None, encoder="sort"):
+    m = Merged(wl.graphs, len(wl.types))
+    pr = wl.priority if priority is None else priority
+    return m, S.fsm_schedule(m, S.table_from_priority(pr, len(wl.types)), encoder)
+
+
+def _check_schedule(wl, priority=None):
+    plan = _plan(wl, priority=priority)
+    m, so = _oracle_schedule(wl, priority)
+    sc = plan.schedule()
+    assert [(t, sorted(b)) for t, b in sc] == so
+    assert plan.info["lower_bound"] == lower_bound_dp(m)
+    assert plan.info["num_batches"] == len(so)
+    return plan, m, so
+
+
+@pytest.mark.parametrize("wlf", [
+    lambda: W.config("cfg1"),
+    lambda: W.treelstm(32, (1, 30), 64, "bf16", cfg=9),
+    lambda: W.treelstm(20, (1, 25), 64, "fp32", cfg=10, cell="treegru"),
+    lambda: W.treefc(40, (1, 30), 64, "bf16", cfg=4),
+    lambda: W.bilstm(16, (1, 20), 64, "bf16", with_tagger=False),
+])
+def test_schedule_bit_exact_with_oracle(wlf):
+    _check_schedule(wlf())
+
+
+def test_schedule_bit_exact_cfg3_full_size():
+    _check_schedule(W.config("cfg3"))
+
+
+def test_schedule_all_priorities_tiny_trees():
+    wl = W.treelstm(3, (2, 6), 32, "fp32", cfg=21)
+    for pr in ([0, 1, 2], [2, 1, 0], [1, 0, 2], [0, 2, 1], [1, 2, 0], [2, 0, 1]):
+        _check_schedule(wl, priority=pr)
+
+
+def _fixture_types(names, h=32):
+    kinds = {"I": ("treefc_internal", 2), "O": ("linear_out", 1), "R": ("treefc_internal", 2),
+             "A": ("linear_out", 1), "alpha": ("treefc_internal", 2), "sigma": ("linear_out", 1)}
+    return [W.OpType(n, kinds[n][0], kinds[n][1], weight_set=i, hidden=h, out_dim=4 if kinds[n][0] == "linear_out" else 0,
+                     dtype="fp32") for i, n in enumerate(names)]
+
+
+def test_fig1_fixture_through_the_abi():
+    g, names = W.fig1_fixture()
+    types = _fixture_types(names)
+    plan = E.ed_plan([g], types, E.fsm_from_priority([0, 2, 1], 3))
+    sc = plan.schedule()
+    assert len(sc) == 10 == plan.info["lower_bound"]           # PAPER Fig. 2 / App. B.3
+    assert sum(1 for t, _ in sc if t == 1) == 1                 # all O in one batch
+
+
+def _random_typed_dag(rng, n):
+    """Random DAG whose types have fixed arity: 0,1 -> 2 slots, 2 -> 1 slot (node or external)."""
+    types, ins = [], []
+    for v in range(n):
+        t = rng.randint(0, 2)
+        k = 2 if t < 2 else 1
+        slots = []
+        for _ in range(k):
+            if v > 0 and rng.uniform01() < 0.8:
+                slots.append(rng.randint(0, v - 1))
+            else:
+                slots.append(-1 - rng.randint(0, 9))
+        types.append(t)
+        ins.append(slots)
+    return W.graph_from_lists(types, ins)
+
+
+def test_random_dags_schedule_and_layout_match_oracle():
+    rng = W.SplitMix64(123)
+    types = [W.OpType("A", "treefc_internal", 2, weight_set=0, hidden=32, dtype="fp32"),
+             W.OpType("B", "treefc_internal", 2, weight_set=1, hidden=32, dtype="fp32"),
+             W.OpType("C", "linear_out", 1, weight_set=2, hidden=32, out_dim=3, dtype="fp32")]
+    for trial in range(25):
+        graphs = [_random_typed_dag(rng, rng.randint(1, 25)) for _ in range(rng.randint(1, 4))]
+        wl = W.Workload("rand", types, graphs, [0, 1, 2], [], "fp32", 32)
+        for pr in ([0, 1, 2], [2, 0, 1]):
+            plan = _plan(wl, priority=pr)
+            m, so = _oracle_schedule(wl, pr)
+            assert [(t, sorted(b)) for t, b in plan.schedule()] == so
+            row = plan.layout()
+            assert list(row) == OL.schedule_order_layout(m, so)
+            # CONTIG flags of the lowering == the oracle's ideal-layout check per fixed slot
+            modes = plan.slot_modes()
+            rep = OL.check_ideal(m, so, row)
+            for b, item in enumerate(rep):
+                assert item["result"]
+                for j, ok in enumerate(item["sources"][:2]):
+                    assert bool(modes[b, j]) == ok
+
+
+def test_schedule_order_layout_results_contiguous_and_members_by_row():
+    wl = W.treelstm(10, (2, 12), 32, "fp32", cfg=3)
+    plan = _plan(wl)
+    row = plan.layout()
+    for t, mem in plan.schedule():
+        rows = [row[v] for v in mem]
+        assert rows == list(range(rows[0], rows[0] + len(rows)))
+
+
+def test_plan_info_fields():
+    wl = W.config("cfg1")
+    plan = _plan(wl)
+    i = plan.info
+    assert i["num_nodes"] == wl.num_nodes and i["num_rows"] == wl.num_nodes + 1
+    assert i["num_instances"] == len(wl.graphs) and i["hidden"] == 32 and i["dtype"] == E.ED_FP32
+    assert i["workspace_bytes"] >= i["off_y"] + 4 * i["num_rows"] * i["y_cols"]
+    assert i["off_h"] % 1024 == 0 and i["off_c"] % 1024 == 0
+    assert i["contig_operands"] + i["gather_operands"] > 0
+    assert i["plan_us"] > 0
+
+
+def _expect(code, fn):
+    with pytest.raises(E.EdError) as ei:
+        fn()
+    assert ei.value.name == code, str(ei.value)
+
+
+def test_error_codes():
+    t = [W.OpType("I", "treefc_internal", 2, weight_set=0, hidden=64, dtype="bf16")]
+    fsm = E.fsm_from_priority([0], 1)
+    cyc = W.graph_from_lists([0, 0], [[1, -1], [0, -1]])
+    _expect("ED_E_CYCLE", lambda: E.ed_plan([cyc], t, fsm))
+    dang = W.graph_from_lists([0], [[5, -1]])
+    _expect("ED_E_DANGLING", lambda: E.ed_plan([dang], t, fsm))
+    arity = W.graph_from_lists([0], [[-1]])
+    _expect("ED_E_ARITY", lambda: E.ed_plan([arity], t, fsm))
+    badt = W.graph_from_lists([3], [[-1, -2]])
+    _expect("ED_E_TYPE", lambda: E.ed_plan([badt], t, fsm))
+    ok = W.graph_from_lists([0], [[-1, -2]])
+    _expect("ED_E_FSM", lambda: E.ed_plan([ok], t, [((0,), 1)]))          # action not in key
+    t2 = t + [W.OpType("J", "treefc_internal", 2, weight_set=1, hidden=64, dtype="bf16")]
+    _expect("ED_E_FSM", lambda: E.ed_plan([ok], t2, [((0, 0), 0)]))      # repeated type in key
+    _expect("ED_E_FSM", lambda: E.ed_plan([ok], t2, [((0, 7), 0)]))      # type out of range
+    odd = [W.OpType("I", "treefc_internal", 2, weight_set=0, hidden=48, dtype="bf16")]
+    _expect("ED_E_TYPE", lambda: E.ed_plan([ok], odd, fsm))              # bf16 needs h % 64 == 0
+    mix = [t[0], W.OpType("J", "treefc_internal", 2, weight_set=1, hidden=128, dtype="bf16")]
+    _expect("ED_E_TYPE", lambda: E.ed_plan([ok], mix, E.fsm_from_priority([0, 1], 2)))
+
+
+def test_null_arguments_rejected():
+    out = ctypes.c_void_p()
+    assert E.LIB.ed_plan(None, 1, None, 1, None, None, ctypes.byref(out)) == -1
+    assert E.LIB.ed_plan_info(None, None) == -1
+    assert b"bad" in E.LIB.ed_last_error() or len(E.LIB.ed_last_error()) > 0
+
+
+def test_fsm_table_miss_falls_back_to_key0():
+    wl = W.treelstm(6, (2, 9), 32, "fp32", cfg=5)
+    plan = E.ed_plan(wl.graphs, wl.types, [])          # every lookup misses
+    m = Merged(wl.graphs, 3)
+    so = S.fsm_schedule(m, {})
+    assert [(t, sorted(b)) for t, b in plan.schedule()] == so
+
+
+def test_packed_bytes():
+    h = 512
+    assert E.ed_packed_bytes("treelstm_internal", h, 0, "bf16", 0) == 5 * h * 2 * h * 2
+    assert E.ed_packed_bytes("treelstm_leaf", h, 0, "fp32", 0) == 3 * h * h * 4
+    assert E.ed_packed_bytes("linear_out", h, 5, "bf16", 0) == 5 * h * 4
+
+
+def test_empty_and_degenerate_graphs():
+    t = [W.OpType("I", "treefc_internal", 2, weight_set=0, hidden=64, dtype="bf16")]
+    fsm = E.fsm_from_priority([0], 1)
+    empty = W.Graph(np.zeros(0, np.int32), np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32), -5)
+    one = W.graph_from_lists([0], [[-1, -2]])
+    plan = E.ed_plan([empty, one, empty], t, fsm)
+    assert plan.info["num_nodes"] == 1 and plan.info["num_batches"] == 1 and plan.info["num_instances"] == 3

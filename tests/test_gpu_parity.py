@@ -1,0 +1,97 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star; metric = DESIGN.md reading A-19): max relative error
+<= 1e-4 for the fp32 path and <= 2e-2 for the bf16 path, per output tensor (h, c, logits, roots).
+Sizes span several 128-row tiles with a ragged tail; the BASELINE full size (cfg3) is checked on
+a sampled set of instances in the exact launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from harness import TOL, compare, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(wl, instances=None, layout=0):
+    plan, w, ws, out = run_gpu(wl, layout=layout)
+    err = compare(wl, plan, ws, out, instances)
+    tol = TOL[wl.dtype]
+    assert all(v <= tol for v in err.values()), err
+    return plan, w, ws, out, err
+
+
+def test_cfg1_treelstm_h32_fp32_all_nodes():
+    _check(W.config("cfg1"))
+
+
+@pytest.mark.parametrize("h", [64, 128, 256])
+def test_treelstm_bf16_ragged_tiles(h):
+    # ~40 trees -> batches of 1..~600 rows: several tiles plus ragged tails and m = 1 steps
+    _check(W.treelstm(40, (1, 30), h, "bf16", cfg=30 + h))
+
+
+def test_treelstm_fp32_h64():
+    _check(W.treelstm(24, (1, 20), 64, "fp32", cfg=31))
+
+
+def test_cfg3_full_size_sampled_instances():
+    wl = W.config("cfg3")
+    sizes = [g.num_nodes for g in wl.graphs]
+    tallest = list(np.argsort(sizes)[-8:])
+    rng = np.random.default_rng(7)
+    rest = list(rng.choice(len(wl.graphs), 24, replace=False))
+    _check(wl, sorted(set(int(x) for x in tallest + rest)))
+
+
+@pytest.mark.parametrize("dtype,h", [("bf16", 128), ("fp32", 64)])
+def test_treegru(dtype, h):
+    _check(W.treelstm(24, (1, 24), h, dtype, cfg=40, cell="treegru"))
+
+
+@pytest.mark.parametrize("dtype,h", [("bf16", 128), ("fp32", 64)])
+def test_treefc_with_external_leaves_and_single_leaf_instances(dtype, h):
+    wl = W.treefc(30, (1, 24), h, dtype, cfg=41)
+    # a 1-leaf instance has no ops; its output is the external (word) row itself
+    wl.graphs.insert(3, W.Graph(np.zeros(0, np.int32), np.zeros(1, np.int32), np.zeros(0, np.int32),
+                                np.zeros(0, np.int32), -1 - 17))
+    _check(wl)
+
+
+@pytest.mark.parametrize("dtype,h", [("bf16", 128), ("fp32", 64)])
+def test_bilstm_chains(dtype, h):
+    _check(W.bilstm(20, (1, 30), h, dtype, cfg=42, with_tagger=False))
+
+
+def test_single_node_and_single_leaf_trees():
+    wl = W.treelstm(9, (1, 1), 64, "bf16", cfg=43)   # every instance: one leaf + its O
+    _check(wl)
+
+
+def test_repeat_execute_is_bitwise_deterministic():
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.treelstm(30, (2, 25), 128, "bf16", cfg=44)
+    plan, w, ws, out = run_gpu(wl)
+    h1 = ws.H().clone(); c1 = ws.C().clone(); y1 = ws.Y().clone()
+    E.ed_execute(plan, w, ws, out)
+    torch.cuda.synchronize()
+    assert torch.equal(h1, ws.H()) and torch.equal(c1, ws.C()) and torch.equal(y1, ws.Y())
+
+
+def test_step_timestamps_cover_every_batch():
+    wl = W.treelstm(16, (2, 16), 64, "bf16", cfg=45)
+    plan, w, ws, out = run_gpu(wl)
+    dt = ws.step_times_ns()
+    assert len(dt) == plan.info["num_batches"] and np.all(dt > 0)
+
+
+def test_workspace_too_small_is_rejected():
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.treelstm(4, (2, 5), 64, "bf16", cfg=46)
+    plan, w, ws, out = run_gpu(wl)
+    ws.nbytes = plan.info["workspace_bytes"] - 1024
+    with pytest.raises(E.EdError) as ei:
+        E.ed_execute(plan, w, ws, out)
+    assert ei.value.name == "ED_E_WORKSPACE"

@@ -157,8 +157,9 @@ def tree_graph(n_leaves: int, rng: SplitMix64, tok: SplitMix64, vocab: int,
     return b.build(root)
 
 
-def bichain_graph(length: int, tok: SplitMix64, vocab: int, t_f: int, t_b: int, t_t: int) -> Graph:
-    """BiChain(L): forward chain F_0..F_{L-1}, backward chain B_{L-1}..B_0, tagger T_t(F_t, B_t)."""
+def bichain_graph(length: int, tok: SplitMix64, vocab: int, t_f: int, t_b: int, t_t: Optional[int]) -> Graph:
+    """BiChain(L): forward chain F_0..F_{L-1}, backward chain B_{L-1}..B_0, tagger T_t(F_t, B_t)
+    (t_t None: no tagger ops; the root is then F_{L-1})."""
     b = _GraphBuilder()
     tokens = [tok.randint(0, vocab - 1) for _ in range(length)]
     f_ids, b_ids = [], [None] * length
@@ -170,9 +171,10 @@ def bichain_graph(length: int, tok: SplitMix64, vocab: int, t_f: int, t_b: int, 
     for t in range(length - 1, -1, -1):
         prev = b.add(t_b, [prev], tokens[t])
         b_ids[t] = prev
-    last = -1
-    for t in range(length):
-        last = b.add(t_t, [f_ids[t], b_ids[t]])
+    last = f_ids[-1]
+    if t_t is not None:
+        for t in range(length):
+            last = b.add(t_t, [f_ids[t], b_ids[t]])
     return b.build(last)
 
 
@@ -340,19 +342,21 @@ def treefc(n_trees: int, leaves: tuple, h: int, dtype: str, cfg: int, vocab: int
 
 
 def bilstm(n_seqs: int, lengths: tuple, h: int, dtype: str, cfg: int = 2, vocab: int = 10000,
-           out_dim: int = 9) -> Workload:
+           out_dim: int = 9, with_tagger: bool = True) -> Workload:
     """BiLSTM tagger: types F, B (LSTM cells, separate weights) and T (tagger MLP)."""
     rng = SplitMix64(1000 + cfg)
     tok = SplitMix64(3000 + cfg)
     types = [OpType("F", "lstm", 1, has_ext=1, weight_set=0, hidden=h, dtype=dtype),
              OpType("B", "lstm", 1, has_ext=1, weight_set=1, hidden=h, dtype=dtype),
              OpType("T", "tagger", 2, weight_set=2, hidden=h, out_dim=out_dim, dtype=dtype)]
-    graphs = [bichain_graph(rng.randint(lengths[0], lengths[1]), tok, vocab, 0, 1, 2)
+    graphs = [bichain_graph(rng.randint(lengths[0], lengths[1]), tok, vocab, 0, 1, 2 if with_tagger else None)
               for _ in range(n_seqs)]
+    if not with_tagger:
+        types = types[:2]
     gen = np.random.default_rng(2000 + cfg)
     params = [make_params("lstm", h, gen, vocab=vocab), make_params("lstm", h, gen, vocab=vocab),
-              make_params("tagger", h, gen, out_dim=out_dim)]
-    return Workload(name=f"bilstm_h{h}_{dtype}", types=types, graphs=graphs, priority=[0, 1, 2],
+              make_params("tagger", h, gen, out_dim=out_dim)][:len(types)]
+    return Workload(name=f"bilstm_h{h}_{dtype}", types=types, graphs=graphs, priority=list(range(len(types))),
                     params=_finish_params(params, dtype), dtype=dtype, hidden=h,
                     config={"instances": n_seqs, "lengths": list(lengths), "cfg": cfg})
 
