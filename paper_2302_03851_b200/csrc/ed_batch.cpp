@@ -372,7 +372,7 @@ static ed_status_t lower(ed_plan_t *pl) {
     st.var_off = -1;
     st.gates = ed::cell_gates(ot.cell_kind);
     st.units = ed::cell_units(ot.cell_kind);
-    st.n_col_tiles = st.units > 0 ? h / st.units : 0;
+    st.n_col_tiles = st.units > 0 ? (h + st.units - 1) / st.units : 0;
     st.nslots = std::min(ot.num_slots, ed::kMaxSlotsDev);
     for (int j = 0; j < st.nslots; ++j) {
       std::vector<int32_t> ent(m);

@@ -91,15 +91,16 @@ inline int cell_gates(int cell) {
   }
 }
 
-// Hidden units per column tile on the bf16 tensor-core path (N tile = gates * units <= 256).
-// Fixed per cell kind so that host tiling and the device epilogue templates agree.
+// Hidden units per column tile on the bf16 tensor-core path (N tile = gates * units <= 256); the
+// last column tile of a row holds the remaining h % units units.  Fixed per cell kind so that host
+// tiling and the device epilogue templates agree.
 inline int cell_units(int cell) {
   switch (cell) {
-    case ED_CELL_TREELSTM_LEAF: return 64;      // N = 192
-    case ED_CELL_TREELSTM_INTERNAL: return 32;  // N = 160
-    case ED_CELL_TREEGRU_LEAF: return 64;       // N = 128
-    case ED_CELL_TREEGRU_INTERNAL: return 32;   // N = 160
-    case ED_CELL_TREEFC_INTERNAL: return 64;    // N = 64
+    case ED_CELL_TREELSTM_LEAF: return 80;      // N = 240
+    case ED_CELL_TREELSTM_INTERNAL: return 48;  // N = 240
+    case ED_CELL_TREEGRU_LEAF: return 128;      // N = 256
+    case ED_CELL_TREEGRU_INTERNAL: return 48;   // N = 240
+    case ED_CELL_TREEFC_INTERNAL: return 256;   // N = 256
     case ED_CELL_LSTM: return 64;               // N = 256
     case ED_CELL_LATTICE_CHAR: return 64;       // N = 256
     default: return 0;

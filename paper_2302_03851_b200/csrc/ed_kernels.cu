@@ -11,8 +11,8 @@
 //     warps 0-3  epilogue: tcgen05.ld TMEM -> registers, gates in fp32, vector stores
 //     warp  4    MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128)
 //     warp  5    weight loader: cp.async.bulk of pre-swizzled weight tiles (complete_tx)
-//     warps 6-7  operand loaders: TMA 128-row box for CONTIG operands, 16 B cp.async row gathers
-//                otherwise, into 128B-swizzled A tiles
+//     warps 6-11 operand loaders: TMA 128-row box for CONTIG operands, 16 B cp.async row gathers
+//                otherwise (192 threads), into 128B-swizzled A tiles
 //     4-stage smem ring (mbarrier full/empty), 2 TMEM accumulators (2 x 256 columns).
 //     Narrow cells (output linear, N = C) run as a warp-per-row SIMT phase (HBM-bound).
 //   fp32 path (ed_persistent_f32): FFMA SIMT for every cell (1e-4 parity path; single-pass TF32
@@ -28,7 +28,9 @@ namespace ed {
 // ------------------------------------------------------------------------------------------------
 // constants of the bf16 tensor-core engine
 // ------------------------------------------------------------------------------------------------
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;        // fp32 SIMT kernel
+constexpr int kThreadsTC = 384;      // bf16 tensor-core kernel: 4 epilogue, MMA, B, 6 A-loader warps
+constexpr int kLoaderThreads = 192;  // warps 6..11
 constexpr int kStages = 4;
 constexpr int kTileM = 128;
 constexpr int kChunkK = 64;                  // bf16 elements per 128 B swizzle row
@@ -135,6 +137,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
 }
+// 32 lanes x 32 bit, 8 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart (SBO), version 1.
@@ -150,24 +161,27 @@ __device__ __forceinline__ uint32_t idesc_bf16(int n) {
 }
 
 // Grid-wide barrier between dependent batches.  Arrivals: one acq_rel atomic per CTA on a counter;
-// the last arriver publishes the epoch to a per-CTA flag (one 256 B line per CTA, so the waiting
-// CTAs poll 148 different L2 lines instead of hammering one).  Flag value = launch_id << 16 | epoch,
-// so flags left by earlier launches never match.
+// the last arriver's warp 0 publishes the epoch to a per-CTA flag (one 256 B line per CTA, so the
+// waiting CTAs poll 148 different L2 lines instead of hammering one).  Flag value =
+// launch_id << 16 | epoch, so flags left by earlier launches never match.
 __device__ __forceinline__ void grid_sync(unsigned int *bar, unsigned int launch_id, unsigned int &epoch) {
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     ++epoch;
     const unsigned int target = epoch * gridDim.x;
     const unsigned int want = (launch_id << 16) | epoch;
     unsigned int *flags = bar + 64;
-    __threadfence();
-    unsigned int old;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    unsigned int old = 0;
+    if (threadIdx.x == 0)  // acq_rel: releases this CTA's writes, acquires every earlier arrival
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    old = __shfl_sync(0xffffffffu, old, 0);
     if (old == target - 1) {
-      __threadfence();  // one release fence, then relaxed flag stores (release pattern)
-      for (unsigned int c = 0; c < gridDim.x; ++c)
+      // last arriver: warp 0 publishes the epoch to every CTA's flag line (release pattern:
+      // the acquire of the RMW chain, then a fence, then relaxed stores)
+      __threadfence();
+      for (unsigned int c = threadIdx.x; c < gridDim.x; c += 32)
         asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + c * 64), "r"(want) : "memory");
-    } else {
+    } else if (threadIdx.x == 0) {
       unsigned int v, spins = 0;
       while (true) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + blockIdx.x * 64) : "memory");
@@ -538,75 +552,91 @@ __device__ __forceinline__ bool is_umma_cell(int cell) {
 }
 
 // Per-cell configuration of the tensor-core epilogue: G gates, U units per column tile (must
-// match ed::cell_units), NAUX fp32 rows of C prefetched per member (children / previous state).
+// match ed::cell_units; N = G*U <= 256), NAUX fp32 rows of C read per member (children / previous state).
 template <int CELL> struct CellCfg;
-template <> struct CellCfg<ED_CELL_TREELSTM_LEAF> { static constexpr int G = 3, U = 64, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TREELSTM_INTERNAL> { static constexpr int G = 5, U = 32, NAUX = 2; };
-template <> struct CellCfg<ED_CELL_TREEGRU_LEAF> { static constexpr int G = 2, U = 64, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TREEGRU_INTERNAL> { static constexpr int G = 5, U = 32, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1, U = 64, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREELSTM_LEAF> { static constexpr int G = 3, U = 80, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREELSTM_INTERNAL> { static constexpr int G = 5, U = 48, NAUX = 2; };
+template <> struct CellCfg<ED_CELL_TREEGRU_LEAF> { static constexpr int G = 2, U = 128, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREEGRU_INTERNAL> { static constexpr int G = 5, U = 48, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1, U = 256, NAUX = 0; };
 template <> struct CellCfg<ED_CELL_LSTM> { static constexpr int G = 4, U = 64, NAUX = 1; };
 template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NAUX = 1; };
+
+// Hidden units of column tile ct (the last tile of a row may be narrower: h need not divide by U).
+__device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { return min(st.units, h - ct * st.units); }
 
 __device__ __forceinline__ float f4get(const float4 &v, int k) {
   return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 
-// Epilogue of one 128 x (G*U) tile for thread r (= TMEM lane = tile row): prefetch the child /
-// previous-state C rows, wait for the accumulator, then per 16 units: tcgen05.ld -> gates (fp32,
-// MUFU tanh.approx) -> bf16 h and fp32 c vector stores.  Bias comes from shared memory.
+// Epilogue of one 128 x (G*units) tile for thread r (= TMEM lane = tile row): wait for the
+// accumulator, then per 16 units: tcgen05.ld -> gates (fp32, MUFU tanh.approx) -> bf16 h and fp32 c
+// vector stores.  The child / previous-state C rows of the next 16-unit group are prefetched
+// while the current one is processed.  Bias comes from shared memory.
 template <int CELL>
 __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
                                               uint32_t parity, int row_tile, int col_tile, int r,
                                               const float *sbias) {
   using CC = CellCfg<CELL>;
-  constexpr int G = CC::G, U = CC::U, NA = CC::NAUX, QPR = U / 4;
+  constexpr int G = CC::G, UMAX = CC::U, NA = CC::NAUX;
   const int h = p.hidden;
   const int i = row_tile * kTileM + r;
   const bool valid = i < st.m;
-  const int jb = col_tile * U;
+  const int jb = col_tile * st.units;
+  const int ngroups = tile_units(st, h, col_tile) / 16;
   int e0 = p.zero_row, e1 = p.zero_row;
   if (valid && st.nslots > 0) e0 = slot_entry(st, p.idx, 0, i);
   if (valid && st.nslots > 1) e1 = slot_entry(st, p.idx, 1, i);
-  float4 aux[NA > 0 ? NA * QPR : 1];
+  const float4 *cp0 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e0 >= 0 ? e0 : p.zero_row) * h + jb);
+  const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1 >= 0 ? e1 : p.zero_row) * h + jb);
+  // 8-unit steps (two per 16-unit TMEM group): small register footprint with 384 threads
+  float4 nxt[NA > 0 ? 2 * NA : 1];
 #pragma unroll
-  for (int q = 0; q < NA * QPR; ++q) {
-    const int row = q < QPR ? e0 : e1;
-    aux[q] = row >= 0 ? __ldcg(reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(row) * h + jb) + (q % QPR))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  for (int q = 0; q < 2 * NA; ++q) nxt[q] = __ldcg((q < 2 ? cp0 : cp1) + (q & 1));
   mbar_wait(tfull_bar, parity);
   tc_fence_after();
   __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
   const size_t orow = static_cast<size_t>(st.out_row0 + (valid ? i : 0));
+  const int nsteps = ngroups * 2;
+#pragma unroll 1
+  for (int sp = 0; sp < nsteps; ++sp) {
+    const int gq = sp >> 1, half = sp & 1;
+    float4 aux[NA > 0 ? 2 * NA : 1];
 #pragma unroll
-  for (int gq = 0; gq < U / 16; ++gq) {
-    float z[G][16];
+    for (int q = 0; q < 2 * NA; ++q) aux[q] = nxt[q];
+    if (sp + 1 < nsteps) {
 #pragma unroll
-    for (int g = 0; g < G; ++g) tmem_ld16(tacc + static_cast<uint32_t>(gq * G * 16 + g * 16), z[g]);
+      for (int q = 0; q < 2 * NA; ++q) nxt[q] = __ldcg((q < 2 ? cp0 : cp1) + (sp + 1) * 2 + (q & 1));
+    }
+    float z[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) tmem_ld8(tacc + static_cast<uint32_t>(gq * G * 16 + g * 16 + half * 8), z[g]);
     tmem_wait_ld();
     if (!valid) continue;
-    const int j0 = jb + gq * 16;
+    const int j0 = jb + sp * 8;
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-      for (int k = 0; k < 16; ++k) z[g][k] += sbias[g * h + j0 + k];
-    float hv[16], cv[16];
+    for (int g = 0; g < G; ++g) {
+      const float4 b0 = *reinterpret_cast<const float4 *>(sbias + g * h + j0);
+      const float4 b1 = *reinterpret_cast<const float4 *>(sbias + g * h + j0 + 4);
+      z[g][0] += b0.x; z[g][1] += b0.y; z[g][2] += b0.z; z[g][3] += b0.w;
+      z[g][4] += b1.x; z[g][5] += b1.y; z[g][6] += b1.z; z[g][7] += b1.w;
+    }
+    float hv[8], cv[8];
     bool has_c = true, done = false;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int qa = gq * 4 + (k >> 2), ka = k & 3;
+    for (int k = 0; k < 8; ++k) {
+      const int qa = k >> 2, ka = k & 3;
       if constexpr (CELL == ED_CELL_TREELSTM_LEAF) {  // [i;o;u]
         cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
         hv[k] = sigm_fast(z[1 % G][k]) * tanh_fast(cv[k]);
       } else if constexpr (CELL == ED_CELL_TREELSTM_INTERNAL) {  // [i;f_l;f_r;o;u]
-        const float cl = f4get(aux[qa % (NA * QPR)], ka), cr = f4get(aux[(QPR + qa) % (NA * QPR)], ka);
+        const float cl = f4get(aux[qa % (2 * NA)], ka), cr = f4get(aux[(2 + qa) % (2 * NA)], ka);
         cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[4 % G][k]) + sigm_fast(z[1 % G][k]) * cl +
                 sigm_fast(z[2 % G][k]) * cr;
         hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
       } else if constexpr (CELL == ED_CELL_LSTM) {  // [i;f;g;o]
-        const float cp = f4get(aux[qa % (NA * QPR)], ka);
-        cv[k] = sigm_fast(z[1 % G][k]) * cp + sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
+        const float cpv = f4get(aux[qa % (2 * NA)], ka);
+        cv[k] = sigm_fast(z[1 % G][k]) * cpv + sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
         hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
       } else if constexpr (CELL == ED_CELL_TREEGRU_LEAF) {  // [z;n]
         hv[k] = (1.f - sigm_fast(z[0][k])) * tanh_fast(z[1 % G][k]);
@@ -624,24 +654,22 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       }
     }
     if (done) continue;
-    uint32_t packed[8];
+    uint32_t packed[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
       __nv_bfloat162 t = __floats2bfloat162_rn(hv[2 * k], hv[2 * k + 1]);
       packed[k] = *reinterpret_cast<uint32_t *>(&t);
     }
-    uint4 *hd = reinterpret_cast<uint4 *>(H + orow * h + j0);
-    hd[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-    hd[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    *reinterpret_cast<uint4 *>(H + orow * h + j0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
     if (has_c) {
       float4 *cd = reinterpret_cast<float4 *>(p.C + orow * h + j0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) cd[q] = make_float4(cv[4 * q], cv[4 * q + 1], cv[4 * q + 2], cv[4 * q + 3]);
+      cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+      cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid_constant__ KParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stages = smem;
@@ -654,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_c
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 4);  // A TMA-or-nothing arrival + 2 cp.async warps + B loader (expect_tx)
+      mbar_init(full + s, 2 + kLoaderThreads / 32);  // A TMA-or-nothing + loader warps + B (expect_tx)
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -725,9 +753,9 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_c
         }
       } else if (warp == 4) {
         // ---------------- MMA issuer ----------------
-        const uint32_t idesc = idesc_bf16(ncols);
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
           const uint32_t acc = pipe.ti & 1u;
+          const uint32_t idesc = idesc_bf16(st.gates * tile_units(st, h, t % st.n_col_tiles));
           if (lane == 0) {
             mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
             tc_fence_after();
@@ -764,9 +792,10 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_c
               const uint32_t stg = pipe.it % kStages;
               mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
               ED_TRACE(p, s, 24 + (kc & 15), t == (int)blockIdx.x);
-              mbar_arrive_tx(full + stg, static_cast<uint32_t>(ncols) * 128u);
+              const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
+              mbar_arrive_tx(full + stg, nb);
               const uint8_t *src = Wp + ((static_cast<size_t>(kc) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-              bulk_g2s(stages + stg * kStageBytes + kAStage, src, static_cast<uint32_t>(ncols) * 128u, full + stg);
+              bulk_g2s(stages + stg * kStageBytes + kAStage, src, nb, full + stg);
               ++pipe.it;
             }
           }
@@ -778,14 +807,14 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_c
         // A gathered operand is fetched with 16 B cp.async per (row, chunk) from a per-tile table of
         // row pointers (H rows or embedding rows); measured on B200 this beats TMA tile::gather4 for
         // 128 B rows.  Each stage is released to the MMA with a lag of kLag stages.
-        const int lt = tid - 192;
+        const int lt = tid - 192;  // 0 .. kLoaderThreads-1
         const int nseg = cell_segments_dev(st.cell);
         asm volatile("fence.proxy.async.global;" ::: "memory");  // H rows of earlier steps: generic -> async proxy
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
           const int row_tile = t / st.n_col_tiles;
           const void **tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
           ++tab_tile;
-          for (int r = lt; r < kTileM; r += 64) {
+          for (int r = lt; r < kTileM; r += kLoaderThreads) {
             const int i = row_tile * kTileM + r;
             const int iv = i < st.m ? i : (st.m - 1);  // rows past m repeat the last valid row
 #pragma unroll
@@ -793,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_c
               tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv))
                                           : p.H;
           }
-          asm volatile("bar.sync 1, 64;" ::: "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
           if (lt == 0) ED_TRACE(p, s, 1, t == (int)blockIdx.x);
           const int nrows = min(kTileM, st.m - row_tile * kTileM);
           for (int kc = 0; kc < kc_total; ++kc) {
@@ -810,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_bf16(const __grid_c
             } else {
               if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
               const uint32_t a_base = smem_u32(a_dst);
-              for (int c = lt; c < nrows * 8; c += 64) {  // rows past m are not loaded
+              for (int c = lt; c < nrows * 8; c += kLoaderThreads) {  // rows past m are not loaded
                 const int r = c >> 3, ch = c & 7;
                 const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
                 cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
@@ -958,7 +987,7 @@ int persistent_grid(int dtype, int *grid) {
   if (dtype == ED_BF16) {
     cudaError_t ce = cudaFuncSetAttribute(ed_persistent_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (ce != cudaSuccess) return static_cast<int>(ce);
-    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ed_persistent_bf16, kThreads, kSmemBytes);
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ed_persistent_bf16, kThreadsTC, kSmemBytes);
     if (ce != cudaSuccess) return static_cast<int>(ce);
     if (per_sm > 1) per_sm = 1;  // TMEM: one 512-column allocation per SM
   } else {
@@ -976,7 +1005,7 @@ int launch_persistent(const KParams &p, int dtype, int grid, void *stream) {
   if (e != cudaSuccess) return static_cast<int>(e);
   void *args[] = {const_cast<KParams *>(&p)};
   if (dtype == ED_BF16) {
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_bf16), dim3(grid), dim3(kThreads), args,
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_bf16), dim3(grid), dim3(kThreadsTC), args,
                                     kSmemBytes, s);
   } else {
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_f32), dim3(grid), dim3(kThreads), args, 0,
