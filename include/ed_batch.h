@@ -127,6 +127,7 @@ typedef struct {
   int64_t num_nodes;          /* V (all instances)                                        */
   int64_t num_instances;
   int64_t num_batches;        /* length of the schedule                                   */
+  int64_t num_steps;          /* device steps (a two-contraction cell = 2 steps per batch) */
   int64_t lower_bound;        /* sum_t Depth(G_t) (App. B.3)                   */
   int64_t num_rows;           /* V + 1 (row V is the all-zero row)                        */
   int64_t hidden;
@@ -141,7 +142,7 @@ typedef struct {
   int64_t off_y;              /*   Y [num_rows x y_cols] f32 (logits of output ops)       */
   int64_t y_cols;
   int64_t off_x;              /*   X [num_rows x hidden] f32 (lattice link gates)         */
-  int64_t off_ts;             /*   u64 %globaltimer stamp after each batch (num_batches+1) */
+  int64_t off_ts;             /*   u64 %globaltimer stamp after each device step (num_steps+1) */
   double plan_us;             /* host time spent in ed_plan                               */
   double schedule_us;
   double layout_us;
@@ -173,7 +174,7 @@ typedef struct {
 typedef struct {
   void *out_root;   /* [num_instances x hidden] in the plan dtype: root h of each instance, in
                        instance order (may be NULL) */
-  uint64_t *trace;  /* optional device buffer [num_batches x 8] of %globaltimer stamps taken by
+  uint64_t *trace;  /* optional device buffer [num_steps x 64] of %globaltimer stamps taken by
                        CTA 0 at fixed phases of each batch (profiling aid; NULL = off) */
 } ed_io_t;
 

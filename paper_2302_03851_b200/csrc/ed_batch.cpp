@@ -343,7 +343,6 @@ static ed_status_t lower(ed_plan_t *pl) {
   const int zero_row = static_cast<int32_t>(V);
   const int nb = static_cast<int>(pl->batch_type.size());
   const int h = pl->hidden;
-  pl->steps.assign(nb, ed::DevStep{});
   pl->idx.clear();
   pl->slot_modes.assign(static_cast<size_t>(nb) * 2, -1);
   pl->contig = pl->gather = pl->copy_bytes = pl->copy_kernels = 0;
@@ -353,6 +352,7 @@ static ed_status_t lower(ed_plan_t *pl) {
     if (x == ED_ZERO_INPUT) return zero_row;
     return x;  // external id
   };
+  pl->steps.clear();
   for (int b = 0; b < nb; ++b) {
     const int t = pl->batch_type[b];
     const ed_op_type_t &ot = pl->types[t];
@@ -360,7 +360,7 @@ static ed_status_t lower(ed_plan_t *pl) {
     std::sort(mem.begin(), mem.end(), [&](int32_t a, int32_t c) { return pl->row_of_node[a] < pl->row_of_node[c]; });
     std::copy(mem.begin(), mem.end(), pl->members.begin() + pl->batch_off[b]);
     const int m = static_cast<int>(mem.size());
-    ed::DevStep &st = pl->steps[b];
+    ed::DevStep st{};
     st.cell = ot.cell_kind;
     st.m = m;
     st.out_row0 = pl->row_of_node[mem[0]];
@@ -370,12 +370,14 @@ static ed_status_t lower(ed_plan_t *pl) {
     st.wset = ot.weight_set;
     st.ext_off = -1;
     st.var_off = -1;
-    st.gates = ed::cell_gates(ot.cell_kind);
+    st.gates = ot.cell_kind == ED_CELL_LINEAR_OUT ? ot.out_dim : ed::cell_gates(ot.cell_kind);
     st.units = ed::cell_units(ot.cell_kind);
     st.n_col_tiles = st.units > 0 ? (h + st.units - 1) / st.units : 0;
     st.nslots = std::min(ot.num_slots, ed::kMaxSlotsDev);
+    std::vector<int32_t> slot_entries[ed::kMaxSlotsDev];
     for (int j = 0; j < st.nslots; ++j) {
-      std::vector<int32_t> ent(m);
+      std::vector<int32_t> &ent = slot_entries[j];
+      ent.resize(m);
       bool contig = true;
       for (int i = 0; i < m; ++i) {
         ent[i] = encode(pl->in_idx[pl->in_off[mem[i]] + j]);
@@ -411,6 +413,34 @@ static ed_status_t lower(ed_plan_t *pl) {
       }
       pl->idx[offs + m] = static_cast<int32_t>(pl->idx.size());
     }
+    pl->steps.push_back(st);
+    // two-contraction cells: the dependent second GEMM is its own device step over the same rows
+    if (ot.cell_kind == ED_CELL_LATTICE_WORD) {
+      ed::DevStep s2 = st;  // l = s(W_l [x_e; c^w] + b_l): x_e = slot 1 (external char), c^w = own row
+      s2.cell = ed::kCellLatticeLink;
+      s2.wsel = 1;
+      s2.ext_off = -1;
+      s2.gates = 1;
+      s2.units = ed::cell_units(s2.cell);
+      s2.n_col_tiles = (h + s2.units - 1) / s2.units;
+      s2.mode[0] = st.mode[1];
+      s2.arg[0] = st.arg[1];
+      s2.mode[1] = 1;
+      s2.arg[1] = st.out_row0;
+      s2.nslots = 2;
+      pl->steps.push_back(s2);
+    } else if (ot.cell_kind == ED_CELL_TAGGER) {
+      ed::DevStep s2 = st;  // y = W2 t + b2 with t in the node's own h row
+      s2.cell = ed::kCellTaggerOut;
+      s2.wsel = 1;
+      s2.gates = ot.out_dim;
+      s2.units = 0;
+      s2.n_col_tiles = 0;
+      s2.mode[0] = 1;
+      s2.arg[0] = st.out_row0;
+      s2.nslots = 1;
+      pl->steps.push_back(s2);
+    }
   }
   pl->root_rows.resize(pl->ninst);
   for (int i = 0; i < pl->ninst; ++i) {
@@ -422,8 +452,9 @@ static ed_status_t lower(ed_plan_t *pl) {
   const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
   size_t off = 0;
   pl->off_bar = off; off += 256 + 256 * 1024;  // counter + per-CTA flags (256 B apart)
-  pl->off_ts = off; off = align_up(off + 8 * static_cast<size_t>(nb + 1), 256);
-  pl->off_steps = off; off = align_up(off + sizeof(ed::DevStep) * nb, 256);
+  const size_t nsteps = pl->steps.size();
+  pl->off_ts = off; off = align_up(off + 8 * (nsteps + 1), 256);
+  pl->off_steps = off; off = align_up(off + sizeof(ed::DevStep) * nsteps, 256);
   pl->off_idx = off; off = align_up(off + 4 * pl->idx.size(), 256);
   pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 1024);
   pl->off_h = off; off = align_up(off + elt * rows * h, 1024);
@@ -440,7 +471,7 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->ws_bytes = off;
   // host blob mirrors [ts .. roots] so one async H2D uploads the static part
   pl->blob.assign(pl->off_h - pl->off_ts, 0);
-  std::memcpy(pl->blob.data() + (pl->off_steps - pl->off_ts), pl->steps.data(), sizeof(ed::DevStep) * nb);
+  std::memcpy(pl->blob.data() + (pl->off_steps - pl->off_ts), pl->steps.data(), sizeof(ed::DevStep) * nsteps);
   if (!pl->idx.empty()) std::memcpy(pl->blob.data() + (pl->off_idx - pl->off_ts), pl->idx.data(), 4 * pl->idx.size());
   if (pl->ninst) std::memcpy(pl->blob.data() + (pl->off_roots - pl->off_ts), pl->root_rows.data(), 4 * pl->ninst);
   return ED_OK;
@@ -518,6 +549,7 @@ ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
   o->num_nodes = pl->V;
   o->num_instances = pl->ninst;
   o->num_batches = static_cast<int64_t>(pl->batch_type.size());
+  o->num_steps = static_cast<int64_t>(pl->steps.size());
   o->lower_bound = pl->lower_bound;
   o->num_rows = pl->V + 1;
   o->hidden = pl->hidden;
@@ -587,7 +619,7 @@ ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, 
   return ED_OK;
 }
 
-int32_t ed_execute_launch_count(const ed_plan_t *pl) { return pl ? 1 : 0; }
+int32_t ed_execute_launch_count(const ed_plan_t *pl) { return pl ? 1 : 0; }  // one persistent kernel
 
 ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, void *ws, size_t ws_bytes,
                        void *stream) {
@@ -642,7 +674,7 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   p.ts = reinterpret_cast<unsigned long long *>(base + pl->off_ts);
   p.out_root = io ? io->out_root : nullptr;
   p.trace = io ? reinterpret_cast<unsigned long long *>(io->trace) : nullptr;
-  p.num_steps = static_cast<int32_t>(pl->batch_type.size());
+  p.num_steps = static_cast<int32_t>(pl->steps.size());
   p.hidden = pl->hidden;
   p.rows = static_cast<int32_t>(pl->V + 1);
   p.zero_row = static_cast<int32_t>(pl->V);

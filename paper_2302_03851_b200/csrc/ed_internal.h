@@ -9,6 +9,10 @@
 namespace ed {
 
 constexpr int kMaxWeightSets = 8;
+
+// Device-only step kinds: the second contraction of a two-GEMM cell runs as its own step.
+constexpr int kCellLatticeLink = 101;  // l = s(W_l [x_e; c^w] + b_l) of LatticeLSTM word cells -> X
+constexpr int kCellTaggerOut = 102;    // y = W2 t + b2 of the BiLSTM tagger (t in the node's H row) -> Y
 constexpr int kMaxSlotsDev = 2;   // fixed slots the device reads (all cells have <= 2)
 
 // One batch of the schedule as the persistent kernel sees it (SoA-friendly 64 B record).
@@ -30,7 +34,8 @@ struct DevStep {
   int32_t n_col_tiles;// UMMA path: hidden / units
   int32_t gates;      // G: gate blocks of the main contraction
   int32_t nslots;     // fixed slots present
-  int32_t pad[2];
+  int32_t wsel;       // 0: weight set W/b, 1: second matrix W2/b2
+  int32_t pad;
 };
 static_assert(sizeof(DevStep) == 64, "DevStep must be 64 bytes");
 
@@ -87,6 +92,7 @@ inline int cell_gates(int cell) {
     case ED_CELL_LATTICE_WORD: return 3;
     case ED_CELL_TAGGER: return 1;
     case ED_CELL_MVRNN_INTERNAL: return 1;
+    case kCellLatticeLink: return 1;
     default: return 0;
   }
 }
@@ -103,6 +109,9 @@ inline int cell_units(int cell) {
     case ED_CELL_TREEFC_INTERNAL: return 256;   // N = 256
     case ED_CELL_LSTM: return 64;               // N = 256
     case ED_CELL_LATTICE_CHAR: return 64;       // N = 256
+    case ED_CELL_LATTICE_WORD: return 80;       // N = 240
+    case kCellLatticeLink: return 256;          // N = 256
+    case ED_CELL_TAGGER: return 256;            // N = 256
     default: return 0;
   }
 }
@@ -116,7 +125,10 @@ inline bool cell_implemented(int cell) {
     case ED_CELL_TREEGRU_LEAF:
     case ED_CELL_TREEGRU_INTERNAL:
     case ED_CELL_TREEFC_INTERNAL:
-    case ED_CELL_LSTM: return true;
+    case ED_CELL_LSTM:
+    case ED_CELL_TAGGER:
+    case ED_CELL_LATTICE_CHAR:
+    case ED_CELL_LATTICE_WORD: return true;
     default: return false;
   }
 }

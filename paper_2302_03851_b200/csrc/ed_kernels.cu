@@ -207,7 +207,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // cell math — one hidden unit, fp32
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ int cell_segments_dev(int cell) {
-  return (cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF || cell == ED_CELL_LINEAR_OUT) ? 1 : 2;
+  return (cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF || cell == ED_CELL_LINEAR_OUT ||
+          cell == kCellTaggerOut) ? 1 : 2;
 }
 
 __device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
@@ -243,6 +244,13 @@ __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+__device__ __forceinline__ const void *step_W(const KParams &p, const DevStep &st) {
+  return st.wsel ? p.w[st.wset].W2 : p.w[st.wset].W;
+}
+__device__ __forceinline__ const float *step_b(const KParams &p, const DevStep &st) {
+  return st.wsel ? p.w[st.wset].b2 : p.w[st.wset].b;
+}
+
 // Pointer to the h-vector an operand entry refers to (row of H, or an external embedding row).
 template <typename T>
 __device__ __forceinline__ const T *entry_row(const KParams &p, const DevWeightSet &w, int e, bool second) {
@@ -266,7 +274,8 @@ __device__ __forceinline__ const T *segment_row(const KParams &p, const DevStep 
     }
     return entry_row<T>(p, w, slot_entry(st, p.idx, 0, i), false);
   }
-  return entry_row<T>(p, w, slot_entry(st, p.idx, s, i), false);
+  // lattice link gate: x_e of the word's end char comes from the char table (emb2)
+  return entry_row<T>(p, w, slot_entry(st, p.idx, s, i), cell == kCellLatticeLink && s == 0);
 }
 
 __device__ __forceinline__ bool ext_first_cell(int cell) {
@@ -340,6 +349,19 @@ __device__ __forceinline__ void cell_epilogue(const KParams &p, const DevStep &s
       hv = act_sig<T>(z[3]) * act_tanh<T>(c);
       break;
     }
+    case ED_CELL_LATTICE_WORD: {  // [i;f;g]: c^w = s(f) c_b + s(i) tanh(g); h row <- c^w (link operand)
+      const int eb = slot_entry(st, p.idx, 0, i);
+      c = act_sig<T>(z[1]) * c_of(p, eb, j) + act_sig<T>(z[0]) * act_tanh<T>(z[2]);
+      hv = c;
+      break;
+    }
+    case kCellLatticeLink:  // l = s(W_l [x_e; c^w] + b_l) -> X
+      p.X[orow * h + j] = act_sig<T>(z[0]);
+      return;
+    case ED_CELL_TAGGER:  // t = tanh(W1 [h_f; h_b] + b1) -> h row (read by the tagger output step)
+      hv = act_tanh<T>(z[0]);
+      has_c = false;
+      break;
     case ED_CELL_LATTICE_CHAR: {  // [i;f;o;g]; variadic words: softmax over {s(i)} U {l_w}
       const int ep = slot_entry(st, p.idx, 0, i);
       const int beg = __ldg(p.idx + st.var_off + i), end = __ldg(p.idx + st.var_off + i + 1);
@@ -374,8 +396,8 @@ __device__ __forceinline__ void cell_epilogue(const KParams &p, const DevStep &s
 template <typename T>
 __device__ void simt_gemm_step(const KParams &p, const DevStep &st) {
   const int h = p.hidden, G = st.gates, NS = cell_segments_dev(st.cell);
-  const DevWeightSet &w = p.w[st.wset];
-  const T *Wt = static_cast<const T *>(w.W);
+  const T *Wt = static_cast<const T *>(step_W(p, st));
+  const float *bias = step_b(p, st);
   const int lane = threadIdx.x & 31;
   const int nub = (h + 31) / 32;
   const long tasks = static_cast<long>(st.m) * nub;
@@ -389,7 +411,7 @@ __device__ void simt_gemm_step(const KParams &p, const DevStep &st) {
     const int jj = act ? j : 0;
     float z[5];
 #pragma unroll
-    for (int g = 0; g < 5; ++g) z[g] = (g < G) ? w.b[g * h + jj] : 0.f;
+    for (int g = 0; g < 5; ++g) z[g] = (g < G) ? bias[g * h + jj] : 0.f;
     for (int s = 0; s < NS; ++s) {
       const T *a = segment_row<T>(p, st, s, i);
       const T *wk = Wt + static_cast<size_t>(s) * h * ldw + jj;
@@ -410,8 +432,9 @@ template <typename T>
 __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
   const int h = p.hidden;
   const DevWeightSet &w = p.w[st.wset];
-  const float *W = static_cast<const float *>(w.W);
-  const int C = p.ycols;
+  const float *W = static_cast<const float *>(step_W(p, st));
+  const float *bias = step_b(p, st);
+  const int C = st.gates;  // logits of this step (out_dim of its op type)
   const int lane = threadIdx.x & 31;
   const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
@@ -435,7 +458,7 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
     }
     if (lane == 0) {
       float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-      for (int c = 0; c < C; ++c) y[c] = acc[c] + w.b[c];
+      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
     }
   }
 }
@@ -443,9 +466,10 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
 // bf16 variant (HBM-bound): W staged in shared memory as [h][C] fp32, each warp streams two rows
 // at a time with 16 B loads (lane owns 8-element chunks lane, lane+32, ...), h % 64 == 0.
 __device__ void simt_linear_out_bf16(const KParams &p, const DevStep &st, float *smem_w) {
-  const int h = p.hidden, C = p.ycols;
+  const int h = p.hidden, C = st.gates;  // logits of this step (out_dim of its op type)
   const DevWeightSet &w = p.w[st.wset];
-  const float *W = static_cast<const float *>(w.W);
+  const float *W = static_cast<const float *>(step_W(p, st));
+  const float *bias = step_b(p, st);
   for (int q = threadIdx.x; q < C * h; q += blockDim.x) smem_w[q] = W[q];  // [c][k]
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -499,7 +523,7 @@ __device__ void simt_linear_out_bf16(const KParams &p, const DevStep &st, float 
       const long i = i0 + r;
       if (lane == 0 && i < st.m) {
         float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-        for (int c = 0; c < C; ++c) y[c] = acc[c] + w.b[c];
+        for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
       }
     }
   }
@@ -527,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_f32(const __grid_co
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[0] = globaltimer();
   for (int s = 0; s < p.num_steps; ++s) {
     const DevStep st = p.steps[s];
-    if (st.cell == ED_CELL_LINEAR_OUT)
+    if (st.cell == ED_CELL_LINEAR_OUT || st.cell == kCellTaggerOut)
       simt_linear_out<float>(p, st);
     else
       simt_gemm_step<float>(p, st);
@@ -548,7 +572,8 @@ struct Pipe {
 __device__ __forceinline__ bool is_umma_cell(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
-         cell == ED_CELL_LATTICE_CHAR;
+         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == kCellLatticeLink ||
+         cell == ED_CELL_TAGGER;
 }
 
 // Per-cell configuration of the tensor-core epilogue: G gates, U units per column tile (must
@@ -560,7 +585,10 @@ template <> struct CellCfg<ED_CELL_TREEGRU_LEAF> { static constexpr int G = 2, U
 template <> struct CellCfg<ED_CELL_TREEGRU_INTERNAL> { static constexpr int G = 5, U = 48, NAUX = 0; };
 template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1, U = 256, NAUX = 0; };
 template <> struct CellCfg<ED_CELL_LSTM> { static constexpr int G = 4, U = 64, NAUX = 1; };
-template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NAUX = 1; };
+template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_LATTICE_WORD> { static constexpr int G = 3, U = 80, NAUX = 0; };
+template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 256, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NAUX = 0; };
 
 // Hidden units of column tile ct (the last tile of a row may be narrower: h need not divide by U).
 __device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { return min(st.units, h - ct * st.units); }
@@ -710,7 +738,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const DevStep st = p.steps[s];
     ED_TRACE(p, s, 0, tid == 0);
     if (!is_umma_cell(st.cell)) {
-      if (st.cell == ED_CELL_LINEAR_OUT) simt_linear_out_bf16(p, st, reinterpret_cast<float *>(stages));
+      if (st.cell == ED_CELL_LINEAR_OUT || st.cell == kCellTaggerOut)
+        simt_linear_out_bf16(p, st, reinterpret_cast<float *>(stages));
       else simt_gemm_step<__nv_bfloat16>(p, st);
     } else {
       const int h = p.hidden;
@@ -720,7 +749,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       const int T = mt * st.n_col_tiles;
       if (warp < 4) {
         // ---------------- epilogue warps ----------------
-        const float *bsrc = p.w[st.wset].b;
+        const float *bsrc = step_b(p, st);
         for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
         asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
@@ -741,8 +770,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
               umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
             case ED_CELL_LSTM:
               umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            default:
+            case ED_CELL_LATTICE_CHAR:
               umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case ED_CELL_LATTICE_WORD:
+              umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            case kCellLatticeLink:
+              umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
+            default:
+              umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
           }
           ED_TRACE(p, s, 5, tid == 0 && t == (int)blockIdx.x);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // h rows are read by TMA in later steps
@@ -783,7 +818,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
       } else if (warp == 5) {
         // ---------------- weight (B) loader ----------------
-        const uint8_t *Wp = static_cast<const uint8_t *>(p.w[st.wset].W);
+        const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
         const size_t ntot = static_cast<size_t>(st.gates) * h;
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
           const int col_tile = t % st.n_col_tiles;
@@ -920,7 +955,7 @@ __global__ void copy_f32_kernel(const float *src, float *dst, long n) {
 static bool umma_cell_host(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
-         cell == ED_CELL_LATTICE_CHAR;
+         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == ED_CELL_TAGGER;
 }
 
 // Logical shape of a cell's matrices (rows, cols).
@@ -952,9 +987,10 @@ int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const f
   if (total == 0) return 0;
   if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) {
     copy_f32_kernel<<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), total);
-  } else if (dtype == ED_BF16 && which == 0 && umma_cell_host(cell)) {
+  } else if (dtype == ED_BF16 && umma_cell_host(cell) && (which == 0 || cell == ED_CELL_LATTICE_WORD)) {
     if (hidden % 64 != 0) return static_cast<int>(cudaErrorInvalidValue);
-    pack_umma_kernel<<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), cell_gates(cell), hidden,
+    const int G = which == 0 ? cell_gates(cell) : 1;  // link gate W_l: one gate block
+    pack_umma_kernel<<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), G, hidden,
                                                 static_cast<int>(cols));
   } else if (dtype == ED_BF16) {
     pack_transpose_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), rows, cols);

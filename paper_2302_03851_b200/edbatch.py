@@ -56,7 +56,7 @@ class ed_plan_opts_t(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
 
 
-_INFO_I64 = ("num_nodes", "num_instances", "num_batches", "lower_bound", "num_rows", "hidden", "dtype",
+_INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bound", "num_rows", "hidden", "dtype",
              "workspace_bytes", "contig_operands", "gather_operands", "copy_bytes", "copy_kernels", "off_h",
              "off_c", "off_y", "y_cols", "off_x", "off_ts")
 
@@ -309,7 +309,7 @@ class Workspace:
 
     def step_times_ns(self) -> np.ndarray:
         i = self.plan_info
-        ts = self._view(i["off_ts"], i["num_batches"] + 1, torch.int64).cpu().numpy()
+        ts = self._view(i["off_ts"], i["num_steps"] + 1, torch.int64).cpu().numpy()
         return np.diff(ts)
 
 

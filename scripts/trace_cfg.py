@@ -8,7 +8,7 @@ from paper_2302_03851_b200 import edbatch as E
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 wl = W.config(name)
 plan, w, ws, out = run_gpu(wl)
-nb = plan.info["num_batches"]
+nb = plan.info["num_steps"]
 tr = torch.zeros(nb * 64, dtype=torch.int64, device="cuda")
 for _ in range(3):
     E.ed_execute(plan, w, ws, out, trace=tr)

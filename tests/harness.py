@@ -43,15 +43,18 @@ def compare(wl, plan, ws, out, instances=None):
     H = ws.H().float().cpu().numpy()
     C = ws.C().cpu().numpy()
     Y = ws.Y().cpu().numpy() if plan.info["y_cols"] else None
-    ys, rs = {"h": [], "c": [], "y": []}, {"h": [], "c": [], "y": []}
+    X = ws.X().cpu().numpy() if ws.X() is not None else None
+    ys, rs = {"h": [], "c": [], "y": [], "l": []}, {"h": [], "c": [], "y": [], "l": []}
     for k, gi in enumerate(idx):
         base = m.base[gi]
         for v, rec in recs[k].items():
             r = row[base + v]
             if rec.get("h") is not None:
                 ys["h"].append(H[r]); rs["h"].append(rec["h"])
-            if rec.get("c") is not None and wl.types[wl.graphs[gi].type[v]].kind not in ("lattice_word",):
+            if rec.get("c") is not None:
                 ys["c"].append(C[r]); rs["c"].append(rec["c"])
+            if rec.get("l") is not None:
+                ys["l"].append(X[r]); rs["l"].append(rec["l"])
             if rec.get("y") is not None:
                 C_ = len(rec["y"])
                 ys["y"].append(Y[r][:C_]); rs["y"].append(rec["y"])

@@ -65,6 +65,27 @@ def test_bilstm_chains(dtype, h):
     _check(W.bilstm(20, (1, 30), h, dtype, cfg=42, with_tagger=False))
 
 
+@pytest.mark.parametrize("dtype,h", [("bf16", 256), ("fp32", 64)])
+def test_bilstm_tagger(dtype, h):
+    _check(W.bilstm(16, (1, 30), h, dtype, cfg=47))
+
+
+def test_cfg2_full_size():
+    _check(W.config("cfg2"))
+
+
+@pytest.mark.parametrize("dtype,h", [("bf16", 128), ("fp32", 64)])
+@pytest.mark.parametrize("priority", [[0, 1], [1, 0]])
+def test_lattice(dtype, h, priority):
+    wl = W.lattice(24, (1, 40), h, dtype, cfg=48, priority=priority)
+    _check(wl)
+
+
+def test_cfg5_full_size_sampled():
+    wl = W.config("cfg5")
+    _check(wl, list(range(0, 512, 9)))
+
+
 def test_single_node_and_single_leaf_trees():
     wl = W.treelstm(9, (1, 1), 64, "bf16", cfg=43)   # every instance: one leaf + its O
     _check(wl)

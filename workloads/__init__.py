@@ -159,7 +159,7 @@ def tree_graph(n_leaves: int, rng: SplitMix64, tok: SplitMix64, vocab: int,
 
 def bichain_graph(length: int, tok: SplitMix64, vocab: int, t_f: int, t_b: int, t_t: Optional[int]) -> Graph:
     """BiChain(L): forward chain F_0..F_{L-1}, backward chain B_{L-1}..B_0, tagger T_t(F_t, B_t)
-    (t_t None: no tagger ops; the root is then F_{L-1})."""
+    (t_t None: no tagger ops).  The instance output (root) is the final forward state F_{L-1}."""
     b = _GraphBuilder()
     tokens = [tok.randint(0, vocab - 1) for _ in range(length)]
     f_ids, b_ids = [], [None] * length
@@ -171,11 +171,10 @@ def bichain_graph(length: int, tok: SplitMix64, vocab: int, t_f: int, t_b: int, 
     for t in range(length - 1, -1, -1):
         prev = b.add(t_b, [prev], tokens[t])
         b_ids[t] = prev
-    last = f_ids[-1]
     if t_t is not None:
         for t in range(length):
-            last = b.add(t_t, [f_ids[t], b_ids[t]])
-    return b.build(last)
+            b.add(t_t, [f_ids[t], b_ids[t]])
+    return b.build(f_ids[-1])
 
 
 def lattice_graph(n_chars: int, rng: SplitMix64, tok: SplitMix64, char_vocab: int, word_vocab: int,
