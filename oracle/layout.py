@@ -78,6 +78,8 @@ def paper_copy_kernels(m: Merged, sched, row: Sequence[int]) -> Tuple[int, int]:
         members = list(members)
         ns = fixed_slots(m, members)
         ops = [[("n", v) for v in members]] + [source_operand(m, members, j) for j in range(ns)]
+        # operands reading external rows / the zero state are not layout variables (A-9)
+        ops = [o for o in ops if all(e is not None and e[0] == "n" for e in o)]
         best = None
         for ref in ops:
             if any(e is None or e[0] != "n" for e in ref):

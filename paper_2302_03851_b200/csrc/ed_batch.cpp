@@ -9,6 +9,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <stdexcept>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -525,7 +526,12 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   if (layout == ED_LAYOUT_PQ) {
     ed::LayoutInput li{pl->V, &pl->gtype, &pl->in_off, &pl->in_idx, &pl->batch_type, &pl->batch_off, &pl->members,
                        &pl->types};
-    pl->row_of_node = ed::plan_layout_pq(li);
+    try {
+      pl->row_of_node = ed::plan_layout_pq(li);
+    } catch (const std::exception &ex) {
+      delete pl;
+      return fail(ED_E_INVALID_ARG, std::string("PQ layout planner internal error: ") + ex.what());
+    }
     if (pl->row_of_node.size() != static_cast<size_t>(pl->V)) { delete pl; return fail(ED_E_UNSUPPORTED, "PQ layout planner not available"); }
   } else {
     pl->row_of_node.assign(pl->V, -1);

@@ -116,3 +116,35 @@ def test_workspace_too_small_is_rejected():
     with pytest.raises(E.EdError) as ei:
         E.ed_execute(plan, w, ws, out)
     assert ei.value.name == "ED_E_WORKSPACE"
+
+
+# ---- PQ-tree layout (ED_LAYOUT_PQ): parity, CONTIG (TMA box) operands, bitwise layout invariance ----
+
+def _node_records(plan, ws):
+    """Per global node id: (h row, c row, y row) read through the plan's layout."""
+    row = plan.layout()
+    H, C, Y = ws.H().float().cpu().numpy(), ws.C().cpu().numpy(), ws.Y().cpu().numpy()
+    return H[row], C[row], Y[row] if Y.size else None
+
+
+@pytest.mark.parametrize("wlf", [
+    lambda: W.bilstm(24, (1, 40), 128, "bf16", cfg=60),
+    lambda: W.bilstm(12, (1, 20), 64, "fp32", cfg=61),
+    lambda: W.lattice(32, (1, 40), 128, "bf16", cfg=62),
+    lambda: W.treelstm(40, (1, 30), 128, "bf16", cfg=63),
+])
+def test_pq_layout_parity_and_bitwise_layout_invariance(wlf):
+    wl = wlf()
+    plan_pq, _, ws_pq, out_pq, _ = _check(wl, layout=1)
+    assert plan_pq.info["contig_operands"] > 0
+    plan_s, _, ws_s, out_s = run_gpu(wl, layout=0)
+    a = _node_records(plan_pq, ws_pq)
+    b = _node_records(plan_s, ws_s)
+    for x, y in zip(a, b):
+        if x is not None:
+            assert np.array_equal(x, y)          # same bits whatever row a node lives in
+    assert torch.equal(out_pq, out_s)
+
+
+def test_cfg2_pq_layout_full_size():
+    _check(W.config("cfg2"), layout=1)
