@@ -27,20 +27,42 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 METRIC = "instances/sec TreeLSTM h=512 (BASELINE cfg3: 256 random trees, bf16) per step, whole job"
+METRICS = {"cfg3": METRIC,
+           "cfg3_gru": "instances/sec TreeGRU h=512 (256 random trees, bf16) per step, whole job",
+           "cfg1": "instances/sec TreeLSTM h=32 (cfg1: 8 random trees, fp32) per step, whole job",
+           "cfg2": "instances/sec BiLSTM-tagger h=256 (cfg2: 64 sequences, bf16) per step, whole job",
+           "cfg5": "instances/sec LatticeLSTM h=256 (cfg5: 512 lattices, bf16) per step, whole job",
+           "cfg4_treefc": "instances/sec TreeFC h=512 (cfg4: 1024 trees, bf16) per step, whole job"}
 CONFIGS = {
     "cfg3": "cfg3 TreeLSTM h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16, FSM L>I>O",
     "cfg3_gru": "cfg3 TreeGRU h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
     "cfg1": "cfg1 TreeLSTM h=32, 8 random trees (leaves U[2,16]), fp32",
+    "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16, FSM F>B>T",
+    "cfg5": "cfg5 LatticeLSTM h=256, 512 character lattices (chars U[10,50], word p=0.3), bf16",
+    "cfg4_treefc": "cfg4 TreeFC h=512, 1024 random trees (leaves U[5,40]), bf16",
 }
 
 
-def make_workload(name: str, rank: int):
+def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
+    """weak: every rank runs its own minibatch of the config's size (rank 0 = the exact config);
+    strong: the config's minibatch is LPT-sharded across ranks by node count."""
+    if scaling == "strong":
+        from paper_2302_03851_b200.sharding import shard_graphs
+        wl = W.config(name)
+        _, wl.graphs = shard_graphs(wl.graphs, rank, world)
+        return wl
     if rank == 0:
         return W.config(name)
     if name in ("cfg3", "cfg3_gru"):
         return W.treelstm(256, (5, 40), 512, "bf16", 3 + 100 * rank, cell="treegru" if name == "cfg3_gru" else "treelstm")
     if name == "cfg1":
         return W.treelstm(8, (2, 16), 32, "fp32", 1 + 100 * rank)
+    if name == "cfg2":
+        return W.bilstm(64, (10, 50), 256, "bf16", 2 + 100 * rank)
+    if name == "cfg5":
+        return W.lattice(512, (10, 50), 256, "bf16", 5 + 100 * rank)
+    if name == "cfg4_treefc":
+        return W.treefc(1024, (5, 40), 512, "bf16", 4 + 100 * rank)
     raise KeyError(name)
 
 
@@ -69,14 +91,22 @@ def step_work(kind: str, m: int, h: int, C: int, elt: int):
         return 2 * m * 2 * h * h, m * (2 * elt * h + elt * h)
     if kind == "lstm":
         return 2 * m * 2 * h * 4 * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h)
+    if kind == "tagger":
+        return 2 * m * 2 * h * h + 2 * m * h * C, m * (2 * elt * h + 4 * C)
+    if kind == "lattice_char":
+        return 2 * m * 2 * h * 4 * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h)
+    if kind == "lattice_word":
+        return 2 * m * 2 * h * 3 * h + 2 * m * 2 * h * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h + 4 * h)
     raise KeyError(kind)
 
 
 def weight_bytes(kind: str, h: int, C: int, elt: int) -> int:
     g = {"treelstm_leaf": (3, 1), "treelstm_internal": (5, 2), "treegru_leaf": (2, 1), "treegru_internal": (5, 2),
-         "treefc_internal": (1, 2), "lstm": (4, 2)}
+         "treefc_internal": (1, 2), "lstm": (4, 2), "tagger": (1, 2), "lattice_char": (4, 2), "lattice_word": (4, 2)}
     if kind == "linear_out":
         return 4 * C * h
+    if kind == "tagger":
+        return elt * 2 * h * h + 4 * h + 4 * C * h + 4 * C
     G, S = g[kind]
     return elt * G * h * S * h + 4 * G * h
 
@@ -186,7 +216,7 @@ def run_reference(args, rank, world):
             times.append(dt)
     ms = 1e3 * sum(times) / len(times)
     v = sample / (ms / 1e3)
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": world,
+    line = {"impl": "reference", "metric": METRICS[args.config], "value": v, "unit": "instances/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIGS[args.config], "sample_instances_per_step": sample},
@@ -205,6 +235,7 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layout", default="schedule", choices=["schedule", "pq"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -227,7 +258,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2302_03851_b200 import edbatch as E
 
-    wl = make_workload(args.config, rank)
+    wl = make_workload(args.config, rank, world, args.scaling)
     layout = E.ED_LAYOUT_PQ if args.layout == "pq" else E.ED_LAYOUT_SCHEDULE_ORDER
     fsm = E.fsm_from_priority(wl.priority, len(wl.types))
     plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout)
@@ -269,7 +300,7 @@ def main():
         t = torch.tensor([ms_local], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    n_inst_total = len(wl.graphs) * world
+    n_inst_total = len(wl.graphs) * world if args.scaling == "weak" else len(W.config(args.config).graphs)
     value = n_inst_total / (ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers: ed_plan + upload + execute + readback
@@ -313,13 +344,13 @@ def main():
                               for (t, mem), r, s_ in zip(plan.schedule(), troof, meas)]}
         cpu_rate, cpu_n, cpu_dt = cpu_oracle_rate(wl, args.cpu_seconds) if world == 1 or rank == 0 else (None, 0, 0)
         line = {
-            "metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRICS[args.config], "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded parse-like trees, random-init weights)",
             "config": {"workload": CONFIGS[args.config], "instances_per_gpu": len(wl.graphs),
                        "nodes_per_gpu": wl.num_nodes, "batches": plan.info["num_batches"],
                        "lower_bound": plan.info["lower_bound"], "layout": args.layout,
-                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world}"},
+                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world} ({args.scaling}; LPT by node count when strong)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
                          "frac": achieved / P, "traffic": traffic,
                          "kernel": "ed_persistent_bf16" if wl.dtype == "bf16" else "ed_persistent_f32",

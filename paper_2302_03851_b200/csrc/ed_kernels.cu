@@ -578,17 +578,20 @@ __device__ __forceinline__ bool is_umma_cell(int cell) {
 
 // Per-cell configuration of the tensor-core epilogue: G gates, U units per column tile (must
 // match ed::cell_units; N = G*U <= 256), NAUX fp32 rows of C read per member (children / previous state).
+// Per-cell configuration of the tensor-core epilogue: G gates, U units per column tile (must
+// match ed::cell_units; N = G*U <= 256), NC fp32 C rows and NH bf16 H rows read per member
+// (children / previous state), prefetched one 8-unit step ahead.
 template <int CELL> struct CellCfg;
-template <> struct CellCfg<ED_CELL_TREELSTM_LEAF> { static constexpr int G = 3, U = 80, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TREELSTM_INTERNAL> { static constexpr int G = 5, U = 48, NAUX = 2; };
-template <> struct CellCfg<ED_CELL_TREEGRU_LEAF> { static constexpr int G = 2, U = 128, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TREEGRU_INTERNAL> { static constexpr int G = 5, U = 48, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1, U = 256, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_LSTM> { static constexpr int G = 4, U = 64, NAUX = 1; };
-template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_LATTICE_WORD> { static constexpr int G = 3, U = 80, NAUX = 0; };
-template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 256, NAUX = 0; };
-template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NAUX = 0; };
+template <> struct CellCfg<ED_CELL_TREELSTM_LEAF> { static constexpr int G = 3, U = 80, NC = 0, NH = 0; };
+template <> struct CellCfg<ED_CELL_TREELSTM_INTERNAL> { static constexpr int G = 5, U = 48, NC = 2, NH = 0; };
+template <> struct CellCfg<ED_CELL_TREEGRU_LEAF> { static constexpr int G = 2, U = 128, NC = 0, NH = 0; };
+template <> struct CellCfg<ED_CELL_TREEGRU_INTERNAL> { static constexpr int G = 5, U = 48, NC = 0, NH = 2; };
+template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
+template <> struct CellCfg<ED_CELL_LSTM> { static constexpr int G = 4, U = 64, NC = 1, NH = 0; };
+template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NC = 1, NH = 0; };
+template <> struct CellCfg<ED_CELL_LATTICE_WORD> { static constexpr int G = 3, U = 80, NC = 1, NH = 0; };
+template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
+template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 
 // Hidden units of column tile ct (the last tile of a row may be narrower: h need not divide by U).
 __device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { return min(st.units, h - ct * st.units); }
@@ -596,17 +599,26 @@ __device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { re
 __device__ __forceinline__ float f4get(const float4 &v, int k) {
   return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
+__device__ __forceinline__ void unpack_bf16x8(const uint4 &v, float *out) {
+  const __nv_bfloat162 *p = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __bfloat1622float2(p[q]);
+    out[2 * q] = f.x;
+    out[2 * q + 1] = f.y;
+  }
+}
 
 // Epilogue of one 128 x (G*units) tile for thread r (= TMEM lane = tile row): wait for the
-// accumulator, then per 16 units: tcgen05.ld -> gates (fp32, MUFU tanh.approx) -> bf16 h and fp32 c
-// vector stores.  The child / previous-state C rows of the next 16-unit group are prefetched
-// while the current one is processed.  Bias comes from shared memory.
+// accumulator, then per 8 units: tcgen05.ld -> gates (fp32, MUFU tanh.approx) -> vector stores.
+// Child / previous-state rows of the next 8-unit step are prefetched while the current one is
+// processed; bias comes from shared memory.
 template <int CELL>
 __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
                                               uint32_t parity, int row_tile, int col_tile, int r,
                                               const float *sbias) {
   using CC = CellCfg<CELL>;
-  constexpr int G = CC::G, UMAX = CC::U, NA = CC::NAUX;
+  constexpr int G = CC::G, NC = CC::NC, NH = CC::NH;
   const int h = p.hidden;
   const int i = row_tile * kTileM + r;
   const bool valid = i < st.m;
@@ -615,12 +627,27 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   int e0 = p.zero_row, e1 = p.zero_row;
   if (valid && st.nslots > 0) e0 = slot_entry(st, p.idx, 0, i);
   if (valid && st.nslots > 1) e1 = slot_entry(st, p.idx, 1, i);
-  const float4 *cp0 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e0 >= 0 ? e0 : p.zero_row) * h + jb);
-  const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1 >= 0 ? e1 : p.zero_row) * h + jb);
-  // 8-unit steps (two per 16-unit TMEM group): small register footprint with 384 threads
-  float4 nxt[NA > 0 ? 2 * NA : 1];
+  if (e0 < 0) e0 = p.zero_row;  // external inputs have no c / h record here
+  if (e1 < 0) e1 = p.zero_row;
+  const float4 *cp0 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e0) * h + jb);
+  const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1) * h + jb);
+  const __nv_bfloat16 *Hb = static_cast<const __nv_bfloat16 *>(p.H);
+  const uint4 *hp0 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e0) * h + jb);
+  const uint4 *hp1 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e1) * h + jb);
+  // lattice char: words ending here (variadic inputs)
+  int wbeg = 0, wend = 0;
+  if constexpr (CELL == ED_CELL_LATTICE_CHAR) {
+    if (valid) {
+      wbeg = __ldg(p.idx + st.var_off + i);
+      wend = __ldg(p.idx + st.var_off + i + 1);
+    }
+  }
+  float4 cn[NC > 0 ? 2 * NC : 1];
+  uint4 hn[NH > 0 ? NH : 1];
 #pragma unroll
-  for (int q = 0; q < 2 * NA; ++q) nxt[q] = __ldcg((q < 2 ? cp0 : cp1) + (q & 1));
+  for (int q = 0; q < 2 * NC; ++q) cn[q] = __ldcg((q < 2 ? cp0 : cp1) + (q & 1));
+#pragma unroll
+  for (int q = 0; q < NH; ++q) hn[q] = __ldcg(q == 0 ? hp0 : hp1);
   mbar_wait(tfull_bar, parity);
   tc_fence_after();
   __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
@@ -629,12 +656,17 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
 #pragma unroll 1
   for (int sp = 0; sp < nsteps; ++sp) {
     const int gq = sp >> 1, half = sp & 1;
-    float4 aux[NA > 0 ? 2 * NA : 1];
+    float4 cc[NC > 0 ? 2 * NC : 1];
+    uint4 hc[NH > 0 ? NH : 1];
 #pragma unroll
-    for (int q = 0; q < 2 * NA; ++q) aux[q] = nxt[q];
+    for (int q = 0; q < 2 * NC; ++q) cc[q] = cn[q];
+#pragma unroll
+    for (int q = 0; q < NH; ++q) hc[q] = hn[q];
     if (sp + 1 < nsteps) {
 #pragma unroll
-      for (int q = 0; q < 2 * NA; ++q) nxt[q] = __ldcg((q < 2 ? cp0 : cp1) + (sp + 1) * 2 + (q & 1));
+      for (int q = 0; q < 2 * NC; ++q) cn[q] = __ldcg((q < 2 ? cp0 : cp1) + (sp + 1) * 2 + (q & 1));
+#pragma unroll
+      for (int q = 0; q < NH; ++q) hn[q] = __ldcg((q == 0 ? hp0 : hp1) + (sp + 1));
     }
     float z[G][8];
 #pragma unroll
@@ -649,48 +681,92 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       z[g][0] += b0.x; z[g][1] += b0.y; z[g][2] += b0.z; z[g][3] += b0.w;
       z[g][4] += b1.x; z[g][5] += b1.y; z[g][6] += b1.z; z[g][7] += b1.w;
     }
-    float hv[8], cv[8];
-    bool has_c = true, done = false;
+    constexpr bool HAS_C = !(CELL == ED_CELL_TREEGRU_LEAF || CELL == ED_CELL_TREEGRU_INTERNAL ||
+                             CELL == ED_CELL_TREEFC_INTERNAL || CELL == ED_CELL_TAGGER);
+    constexpr bool HAS_H = CELL != kCellLatticeLink;
+    float hv[8] = {}, cv[8] = {};
+    float hl[8], hr[8];
+    if constexpr (NH >= 1) unpack_bf16x8(hc[0], hl);
+    if constexpr (NH >= 2) unpack_bf16x8(hc[NH - 1], hr);
+    float aux0[8], aux1[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int qa = k >> 2, ka = k & 3;
-      if constexpr (CELL == ED_CELL_TREELSTM_LEAF) {  // [i;o;u]
-        cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
-        hv[k] = sigm_fast(z[1 % G][k]) * tanh_fast(cv[k]);
-      } else if constexpr (CELL == ED_CELL_TREELSTM_INTERNAL) {  // [i;f_l;f_r;o;u]
-        const float cl = f4get(aux[qa % (2 * NA)], ka), cr = f4get(aux[(2 + qa) % (2 * NA)], ka);
-        cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[4 % G][k]) + sigm_fast(z[1 % G][k]) * cl +
-                sigm_fast(z[2 % G][k]) * cr;
-        hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
-      } else if constexpr (CELL == ED_CELL_LSTM) {  // [i;f;g;o]
-        const float cpv = f4get(aux[qa % (2 * NA)], ka);
-        cv[k] = sigm_fast(z[1 % G][k]) * cpv + sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
-        hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
-      } else if constexpr (CELL == ED_CELL_TREEGRU_LEAF) {  // [z;n]
-        hv[k] = (1.f - sigm_fast(z[0][k])) * tanh_fast(z[1 % G][k]);
-        has_c = false;
-      } else if constexpr (CELL == ED_CELL_TREEFC_INTERNAL) {
-        hv[k] = tanh_fast(z[0][k]);
-        has_c = false;
-      } else {
-        // TreeGRU internal / lattice char: scalar path shared with the SIMT engine
-        float zz[5];
+      aux0[k] = NC >= 1 ? f4get(cc[(k >> 2) % (2 * (NC > 0 ? NC : 1))], k & 3) : 0.f;
+      aux1[k] = NC >= 2 ? f4get(cc[(2 + (k >> 2)) % (2 * (NC > 0 ? NC : 1))], k & 3) : 0.f;
+    }
+    if constexpr (CELL == ED_CELL_LATTICE_CHAR) {
+      // c = sum_w alpha_w c^w + alpha_e tanh(g), alpha = softmax over {s(i)} U {l_w} (A-23); else LSTM
+      float den[8], num[8];
 #pragma unroll
-        for (int g = 0; g < 5; ++g) zz[g] = z[g % G][k];
-        cell_epilogue<__nv_bfloat16>(p, st, i, j0 + k, zz);
-        done = true;
+      for (int k = 0; k < 8; ++k) {
+        const float si = sigm_fast(z[0][k]);
+        const float ei = __expf(si);
+        den[k] = ei;
+        num[k] = ei * tanh_fast(z[3 % G][k]);
+      }
+      for (int w = wbeg; w < wend; ++w) {
+        const int wr = __ldg(p.idx + w);
+        const float4 *xl = reinterpret_cast<const float4 *>(p.X + static_cast<size_t>(wr) * h + j0);
+        const float4 *xc = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(wr) * h + j0);
+        const float4 l0 = __ldcg(xl), l1 = __ldcg(xl + 1), c0 = __ldcg(xc), c1 = __ldcg(xc + 1);
+        const float lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        const float cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float el = __expf(lw[k]);
+          den[k] += el;
+          num[k] += el * cw[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cv[k] = wend > wbeg ? __fdividef(num[k], den[k])
+                            : sigm_fast(z[1 % G][k]) * aux0[k] + sigm_fast(z[0][k]) * tanh_fast(z[3 % G][k]);
+        hv[k] = sigm_fast(z[2 % G][k]) * tanh_fast(cv[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if constexpr (CELL == ED_CELL_TREELSTM_LEAF) {  // [i;o;u]
+          cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
+          hv[k] = sigm_fast(z[1 % G][k]) * tanh_fast(cv[k]);
+        } else if constexpr (CELL == ED_CELL_TREELSTM_INTERNAL) {  // [i;f_l;f_r;o;u]
+          cv[k] = sigm_fast(z[0][k]) * tanh_fast(z[4 % G][k]) + sigm_fast(z[1 % G][k]) * aux0[k] +
+                  sigm_fast(z[2 % G][k]) * aux1[k];
+          hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
+        } else if constexpr (CELL == ED_CELL_LSTM) {  // [i;f;g;o]
+          cv[k] = sigm_fast(z[1 % G][k]) * aux0[k] + sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
+          hv[k] = sigm_fast(z[3 % G][k]) * tanh_fast(cv[k]);
+        } else if constexpr (CELL == ED_CELL_TREEGRU_LEAF) {  // [z;n]
+          hv[k] = (1.f - sigm_fast(z[0][k])) * tanh_fast(z[1 % G][k]);
+        } else if constexpr (CELL == ED_CELL_TREEGRU_INTERNAL) {  // [z;r_l;r_r;a_l;a_r]
+          const float n = tanh_fast(sigm_fast(z[1 % G][k]) * z[3 % G][k] + sigm_fast(z[2 % G][k]) * z[4 % G][k]);
+          const float zz = sigm_fast(z[0][k]);
+          hv[k] = (1.f - zz) * n + zz * (hl[k] + hr[k]);
+        } else if constexpr (CELL == ED_CELL_TREEFC_INTERNAL) {
+          hv[k] = tanh_fast(z[0][k]);
+        } else if constexpr (CELL == ED_CELL_LATTICE_WORD) {  // [i;f;g] -> c^w (fp32 C) and bf16 copy in H
+          cv[k] = sigm_fast(z[1 % G][k]) * aux0[k] + sigm_fast(z[0][k]) * tanh_fast(z[2 % G][k]);
+          hv[k] = cv[k];
+        } else if constexpr (CELL == kCellLatticeLink) {  // l = s(.) -> X
+          cv[k] = sigm_fast(z[0][k]);
+        } else {  // tagger hidden: t = tanh(.) -> H
+          hv[k] = tanh_fast(z[0][k]);
+        }
       }
     }
-    if (done) continue;
-    uint32_t packed[4];
+    if constexpr (HAS_H) {
+      uint32_t packed[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      __nv_bfloat162 t = __floats2bfloat162_rn(hv[2 * k], hv[2 * k + 1]);
-      packed[k] = *reinterpret_cast<uint32_t *>(&t);
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(hv[2 * k], hv[2 * k + 1]);
+        packed[k] = *reinterpret_cast<uint32_t *>(&t);
+      }
+      *reinterpret_cast<uint4 *>(H + orow * h + j0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
     }
-    *reinterpret_cast<uint4 *>(H + orow * h + j0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-    if (has_c) {
-      float4 *cd = reinterpret_cast<float4 *>(p.C + orow * h + j0);
+    if constexpr (HAS_C) {
+      float *dst = (CELL == kCellLatticeLink) ? p.X : p.C;
+      float4 *cd = reinterpret_cast<float4 *>(dst + orow * h + j0);
       cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
       cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
     }

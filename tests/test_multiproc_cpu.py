@@ -1,0 +1,66 @@
+"""Multi-process (N > 1) host path on CPU: world_size-2 gloo group, one process per "GPU".
+
+Each rank takes its LPT shard of the minibatch (paper_2302_03851_b200/sharding.py),
+plans it through the C ABI (ed_plan is host-only), and checks its schedule bit-exactly against the
+oracle on that shard; the ranks then combine counts with all_reduce (SUM) and the step time with
+all_reduce (MAX), as bench.py does over NCCL.
+"""
+import os
+import sys
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import workloads as W
+        from oracle import schedule as S
+        from oracle.graph import Merged
+        from paper_2302_03851_b200 import edbatch as E
+        from paper_2302_03851_b200.sharding import shard_graphs
+        wl = W.treelstm(40, (2, 20), 64, "bf16", cfg=3)
+        idx, graphs = shard_graphs(wl.graphs, rank, world)
+        plan = E.ed_plan(graphs, wl.types, E.fsm_from_priority(wl.priority, 3))
+        m = Merged(graphs, 3)
+        so = S.fsm_schedule(m, S.table_from_priority(wl.priority, 3))
+        ok = [(t, sorted(b)) for t, b in plan.schedule()] == so
+        t = torch.tensor([len(idx), plan.info["num_nodes"], int(ok)], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms = torch.tensor([1.0 + rank])
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        shards = [None] * world
+        dist.all_gather_object(shards, idx)
+        if rank == 0:
+            q.put((t.tolist(), float(ms.item()), shards, wl.num_nodes, len(wl.graphs)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_planning_gloo():
+    pytest.importorskip("paper_2302_03851_b200.edbatch")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    mp.start_processes(_worker, args=(2, port, q), nprocs=2, join=True, start_method="spawn")
+    (n_inst, n_nodes, n_ok), ms, shards, total_nodes, total_inst = q.get(timeout=60)
+    assert n_inst == total_inst and n_nodes == total_nodes and n_ok == 2
+    assert sorted(shards[0] + shards[1]) == list(range(total_inst))
+    assert ms == 2.0
+
+
+def test_lpt_partition_balance():
+    from paper_2302_03851_b200.sharding import lpt_partition
+    sizes = [9, 8, 7, 6, 5, 4, 3, 2, 1]
+    parts = lpt_partition(sizes, 3)
+    loads = [sum(sizes[i] for i in p) for p in parts]
+    assert sorted(i for p in parts for i in p) == list(range(9))
+    assert max(loads) - min(loads) <= max(sizes)
+    assert lpt_partition([5, 5], 4)[2:] == [[], []]
