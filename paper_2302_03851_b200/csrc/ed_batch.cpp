@@ -373,6 +373,15 @@ static ed_status_t lower(ed_plan_t *pl) {
     st.var_off = -1;
     st.gates = ot.cell_kind == ED_CELL_LINEAR_OUT ? ot.out_dim : ed::cell_gates(ot.cell_kind);
     st.units = ed::cell_units(ot.cell_kind);
+    if (st.units > 0 && pl->dtype == ED_BF16) {
+      // narrower column tiles for small batches: the fewest units per tile (multiple of 16, <= the
+      // cell's maximum) whose tile count still fits one wave of 148 CTAs; a tile's time is set by
+      // its K-chunk chain (operand gather), so more concurrent tiles = shorter batch
+      const int mt = (m + 127) / 128;
+      const int umax = st.units;
+      for (int u = umax; u >= 16; u -= 16)
+        if (mt * ((h + u - 1) / u) <= 148) st.units = u;
+    }
     st.n_col_tiles = st.units > 0 ? (h + st.units - 1) / st.units : 0;
     st.nslots = std::min(ot.num_slots, ed::kMaxSlotsDev);
     std::vector<int32_t> slot_entries[ed::kMaxSlotsDev];

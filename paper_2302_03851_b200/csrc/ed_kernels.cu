@@ -593,6 +593,18 @@ template <> struct CellCfg<ED_CELL_LATTICE_WORD> { static constexpr int G = 3, U
 template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 
+// Row pointers (per K segment) of the 128 rows of a row tile; rows past m repeat the last valid row.
+__device__ __forceinline__ void build_row_table(const KParams &p, const DevStep &st, int row_tile, int nseg, int lt,
+                                                const void **tab) {
+  for (int r = lt; r < kTileM; r += kLoaderThreads) {
+    const int i = row_tile * kTileM + r;
+    const int iv = i < st.m ? i : (st.m - 1);
+#pragma unroll
+    for (int sg = 0; sg < 2; ++sg)
+      tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H;
+  }
+}
+
 // Hidden units of column tile ct (the last tile of a row may be narrower: h need not divide by U).
 __device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { return min(st.units, h - ct * st.units); }
 
@@ -808,6 +820,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   Pipe pipe;
   uint32_t tab_tile = 0;        // loader threads: row-table buffer toggle
   uint32_t cp_pending = 0;      // cp.async warp: committed groups not yet released
+  bool tab_prebuilt = false;    // loader threads: next step's first row table already built
+  int b_pre = 0;                // B loader: stages of this step's first tile issued in advance
   if (blockIdx.x == 0 && tid == 0) p.ts[0] = globaltimer();
 
   for (int s = 0; s < p.num_steps; ++s) {
@@ -894,12 +908,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
       } else if (warp == 5) {
         // ---------------- weight (B) loader ----------------
+        // Weights do not depend on earlier batches, so before the grid barrier of this step the
+        // first stages of the next step's first tile are already issued (b_pre of them).
         const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
         const size_t ntot = static_cast<size_t>(st.gates) * h;
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
           const int col_tile = t % st.n_col_tiles;
           if (lane == 0) {
-            for (int kc = 0; kc < kc_total; ++kc) {
+            for (int kc = (t == static_cast<int>(blockIdx.x) ? b_pre : 0); kc < kc_total; ++kc) {
               const uint32_t stg = pipe.it % kStages;
               mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
               ED_TRACE(p, s, 24 + (kc & 15), t == (int)blockIdx.x);
@@ -911,7 +927,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             }
           }
         }
+        b_pre = 0;
+        if (s + 1 < p.num_steps && lane == 0) {
+          const DevStep nx = p.steps[s + 1];
+          if (is_umma_cell(nx.cell) &&
+              static_cast<int>(blockIdx.x) < ((nx.m + kTileM - 1) / kTileM) * nx.n_col_tiles) {
+            const int nkc = (cell_segments_dev(nx.cell) * h) / kChunkK;
+            const int ct = static_cast<int>(blockIdx.x) % nx.n_col_tiles;
+            const uint8_t *Wn = static_cast<const uint8_t *>(step_W(p, nx));
+            const size_t nt = static_cast<size_t>(nx.gates) * h;
+            const uint32_t nb = static_cast<uint32_t>(nx.gates * tile_units(nx, h, ct)) * 128u;
+            for (int kc = 0; kc < min(kStages, nkc); ++kc) {
+              const uint32_t stg = pipe.it % kStages;
+              mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+              mbar_arrive_tx(full + stg, nb);
+              const uint8_t *src =
+                  Wn + ((static_cast<size_t>(kc) * nt + static_cast<size_t>(ct) * nx.gates * nx.units) * 128);
+              bulk_g2s(stages + stg * kStageBytes + kAStage, src, nb, full + stg);
+              ++pipe.it;
+              ++b_pre;
+            }
+          }
+        }
         pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
+        b_pre = __shfl_sync(0xffffffffu, b_pre, 0);
       } else {
         // ---------------- operand (A) loaders: warps 6-7 (64 threads) ----------------
         // A CONTIG operand (layout plan made its rows adjacent and aligned) is one TMA 128-row box.
@@ -923,17 +962,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         asm volatile("fence.proxy.async.global;" ::: "memory");  // H rows of earlier steps: generic -> async proxy
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
           const int row_tile = t / st.n_col_tiles;
-          const void **tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
-          ++tab_tile;
-          for (int r = lt; r < kTileM; r += kLoaderThreads) {
-            const int i = row_tile * kTileM + r;
-            const int iv = i < st.m ? i : (st.m - 1);  // rows past m repeat the last valid row
-#pragma unroll
-            for (int sg = 0; sg < 2; ++sg)
-              tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv))
-                                          : p.H;
+          const void **tab;
+          if (t == static_cast<int>(blockIdx.x) && tab_prebuilt) {
+            tab = rowtab + ((tab_tile - 1) & 1u) * (kTileM * 2);  // built before the last grid barrier
+          } else {
+            tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
+            ++tab_tile;
+            build_row_table(p, st, row_tile, nseg, lt, tab);
+            asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
           }
-          asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
           if (lt == 0) ED_TRACE(p, s, 1, t == (int)blockIdx.x);
           const int nrows = min(kTileM, st.m - row_tile * kTileM);
           for (int kc = 0; kc < kc_total; ++kc) {
@@ -967,6 +1004,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             ++pipe.it;
           }
           if (lt == 0) ED_TRACE(p, s, 2, t == (int)blockIdx.x);
+        }
+        // the row table of the next step's first tile only reads the (static) step table: build it
+        // before the grid barrier
+        tab_prebuilt = false;
+        if (s + 1 < p.num_steps) {
+          const DevStep nx = p.steps[s + 1];
+          if (is_umma_cell(nx.cell) &&
+              static_cast<int>(blockIdx.x) < ((nx.m + kTileM - 1) / kTileM) * nx.n_col_tiles) {
+            const void **ntab = rowtab + (tab_tile & 1u) * (kTileM * 2);
+            ++tab_tile;
+            build_row_table(p, nx, static_cast<int>(blockIdx.x) / nx.n_col_tiles, cell_segments_dev(nx.cell), lt, ntab);
+            asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
+            tab_prebuilt = true;
+          }
         }
         // drain: release every stage still pending in this step
         cp_async_wait<0>();
