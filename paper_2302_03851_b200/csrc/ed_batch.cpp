@@ -137,10 +137,11 @@ struct ed_plan_s {
   std::vector<ed::DevStep> steps;
   std::vector<int32_t> idx;
   std::vector<int32_t> root_rows;
+  std::vector<int32_t> target;  // per row: h x device steps writing it (dataflow readiness)
   int root_wset = 0;
   // workspace layout
-  size_t off_bar = 0, off_ts = 0, off_steps = 0, off_idx = 0, off_roots = 0, off_h = 0, off_c = 0, off_y = 0,
-         off_x = 0, ws_bytes = 0;
+  size_t off_bar = 0, off_ts = 0, off_steps = 0, off_idx = 0, off_roots = 0, off_target = 0, off_ready = 0,
+         off_h = 0, off_c = 0, off_y = 0, off_x = 0, ws_bytes = 0;
   int64_t y_cols = 0;
   bool need_x = false;
   // stats
@@ -452,6 +453,9 @@ static ed_status_t lower(ed_plan_t *pl) {
       pl->steps.push_back(s2);
     }
   }
+  pl->target.assign(V + 1, 0);
+  for (const auto &st : pl->steps)
+    for (int i = 0; i < st.m; ++i) pl->target[st.out_row0 + i] += h;
   pl->root_rows.resize(pl->ninst);
   for (int i = 0; i < pl->ninst; ++i) {
     const int32_t r = pl->roots[i];
@@ -466,7 +470,9 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->off_ts = off; off = align_up(off + 8 * (nsteps + 1), 256);
   pl->off_steps = off; off = align_up(off + sizeof(ed::DevStep) * nsteps, 256);
   pl->off_idx = off; off = align_up(off + 4 * pl->idx.size(), 256);
-  pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 1024);
+  pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 256);
+  pl->off_target = off; off = align_up(off + 4 * static_cast<size_t>(rows), 256);
+  pl->off_ready = off; off = align_up(off + 4 * static_cast<size_t>(rows), 1024);
   pl->off_h = off; off = align_up(off + elt * rows * h, 1024);
   pl->off_c = off; off = align_up(off + 4 * rows * h, 1024);
   pl->y_cols = 0;
@@ -480,10 +486,11 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->off_x = off; if (pl->need_x) off = align_up(off + 4 * rows * h, 1024);
   pl->ws_bytes = off;
   // host blob mirrors [ts .. roots] so one async H2D uploads the static part
-  pl->blob.assign(pl->off_h - pl->off_ts, 0);
+  pl->blob.assign(pl->off_ready - pl->off_ts, 0);
   std::memcpy(pl->blob.data() + (pl->off_steps - pl->off_ts), pl->steps.data(), sizeof(ed::DevStep) * nsteps);
   if (!pl->idx.empty()) std::memcpy(pl->blob.data() + (pl->off_idx - pl->off_ts), pl->idx.data(), 4 * pl->idx.size());
   if (pl->ninst) std::memcpy(pl->blob.data() + (pl->off_roots - pl->off_ts), pl->root_rows.data(), 4 * pl->ninst);
+  std::memcpy(pl->blob.data() + (pl->off_target - pl->off_ts), pl->target.data(), 4 * pl->target.size());
   return ED_OK;
 }
 
@@ -687,6 +694,13 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   p.X = pl->need_x ? reinterpret_cast<float *>(base + pl->off_x) : nullptr;
   p.bar = reinterpret_cast<unsigned int *>(base + pl->off_bar);
   p.ts = reinterpret_cast<unsigned long long *>(base + pl->off_ts);
+  p.ready = reinterpret_cast<int *>(base + pl->off_ready);
+  p.target = reinterpret_cast<const int *>(base + pl->off_target);
+  {  // per launch: readiness counters and step stamps start from zero
+    cudaError_t ce = cudaMemsetAsync(p.ready, 0, 4 * static_cast<size_t>(pl->V + 1), s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(p.ts, 0, 8 * (pl->steps.size() + 1), s);
+    if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("memset: ") + cudaGetErrorString(ce));
+  }
   p.out_root = io ? io->out_root : nullptr;
   p.trace = io ? reinterpret_cast<unsigned long long *>(io->trace) : nullptr;
   p.num_steps = static_cast<int32_t>(pl->steps.size());

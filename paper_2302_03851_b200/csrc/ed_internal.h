@@ -66,7 +66,9 @@ struct alignas(64) KParams {
   unsigned int *bar;          // grid barrier counter (zeroed before launch)
   unsigned long long *ts;     // [num_steps + 1]
   void *out_root;             // [num_inst x hidden] or null
-  unsigned long long *trace;  // [num_steps x 8] phase stamps of CTA 0, or null
+  unsigned long long *trace;  // [num_steps x 64] phase stamps of CTA 0, or null
+  int *ready;                 // [rows] hidden units published per row (zeroed every launch)
+  const int *target;          // [rows] units a row holds when final (h x device steps writing it)
   int32_t num_steps;
   int32_t hidden;
   int32_t rows;

@@ -38,8 +38,10 @@ constexpr int kAStage = kTileM * 128;        // 16 KB
 constexpr int kBStage = 256 * 128;           // 32 KB (N tile <= 256)
 constexpr int kStageBytes = kAStage + kBStage;
 constexpr int kRowTab = kTileM * 2 * 8;      // row pointers per tile (2 segments)
-constexpr int kBiasBytes = 5 * 1024 * 4;          // G * h fp32 (h <= 1024)
-constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kBiasBytes + 256;
+constexpr int kEntTab = 0;
+constexpr int kBiasBytes = 5 * 512 * 4;           // G * h fp32 (G * h <= 2560)
+constexpr int kWoutBytes = 12 * 1024;             // output-linear weights [C][h] fp32 (else read from L2)
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes + kWoutBytes + 256;
 constexpr int kEpiThreads = 128;
 constexpr int kLag = 3;  // cp.async groups in flight before a stage is released (< kStages)
 
@@ -199,6 +201,43 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// ---- dataflow readiness (replaces per-batch grid barriers) ----
+// ready[row] counts hidden units written to the row by finished device steps; target[row] = h x the
+// number of device steps that write it.  A consumer acquires ready[row] >= target[row] before reading
+// the row; a producer publishes with a release-add after its stores.  Rows are only produced by
+// earlier device steps and every warp walks the steps in order, so waiting cannot deadlock.
+__device__ __forceinline__ int ld_acquire_s32(const int *a) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+// A step that reads its own rows (the second contraction of a two-GEMM cell: link gate, tagger
+// output) needs only the units of the earlier writer: target - h.
+__device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep &st) {
+  if (e < 0 || e >= p.rows) return;  // external rows are static
+  int need = __ldg(p.target + e);
+  if (e >= st.out_row0 && e < st.out_row0 + st.m) need -= p.hidden;
+  if (need <= 0) return;
+  unsigned spins = 0;
+  while (ld_acquire_s32(p.ready + e) < need) {
+    if (++spins > (1u << 26)) __trap();  // watchdog
+    __nanosleep(32);
+  }
+}
+// Non-blocking check of a row (same rule as wait_row).
+__device__ __forceinline__ bool row_ready(const KParams &p, int e, const DevStep &st) {
+  if (e < 0 || e >= p.rows) return true;
+  int need = __ldg(p.target + e);
+  if (e >= st.out_row0 && e < st.out_row0 + st.m) need -= p.hidden;
+  return need <= 0 || ld_acquire_s32(p.ready + e) >= need;
+}
+__device__ __forceinline__ void publish_row(const KParams &p, int row, int units) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + row), "r"(units) : "memory");
+}
+__device__ __forceinline__ void stamp_step(const KParams &p, int s) {
+  atomicMax(p.ts + s + 1, globaltimer());
+}
+
 // optional phase trace of CTA 0 (profiling aid)
 #define ED_TRACE(p, s, k, first) \
   do { if ((p).trace && blockIdx.x == 0 && (first)) (p).trace[(s) * 64 + (k)] = globaltimer(); } while (0)
@@ -407,6 +446,10 @@ __device__ void simt_gemm_step(const KParams &p, const DevStep &st) {
   for (long task = gw; task < tasks; task += nw) {
     const int i = static_cast<int>(task / nub);
     const int j = static_cast<int>(task % nub) * 32 + lane;
+    // inputs of member i: slot rows (A operand, c rows) and variadic words
+    for (int sl = 0; sl < st.nslots; ++sl) wait_row(p, slot_entry(st, p.idx, sl, i), st);
+    if (st.var_off >= 0)
+      for (int w = __ldg(p.idx + st.var_off + i); w < __ldg(p.idx + st.var_off + i + 1); ++w) wait_row(p, __ldg(p.idx + w), st);
     const bool act = j < h;
     const int jj = act ? j : 0;
     float z[5];
@@ -416,18 +459,19 @@ __device__ void simt_gemm_step(const KParams &p, const DevStep &st) {
       const T *a = segment_row<T>(p, st, s, i);
       const T *wk = Wt + static_cast<size_t>(s) * h * ldw + jj;
       for (int k = 0; k < h; ++k) {
-        const float av = to_f<T>(a[k]);
+        const float av = to_f<T>(__ldcg(a + k));
 #pragma unroll
         for (int g = 0; g < 5; ++g)
           if (g < G) z[g] = fmaf(av, to_f<T>(wk[static_cast<size_t>(k) * ldw + g * h]), z[g]);
       }
     }
     if (act) cell_epilogue<T>(p, st, i, j, z);
+    __syncwarp();
+    if (lane == 0) publish_row(p, st.out_row0 + i, min(32, h - (j - lane)));
   }
 }
 
-
-// Output linear O (y = W h + b, fp32 logits): warp per row, W fp32 [C x h].
+// Output linear O (y = W h + b, fp32 logits), fp32 path: warp per row, W fp32 [C x h].
 template <typename T>
 __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
   const int h = p.hidden;
@@ -439,12 +483,14 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
   const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
   for (long i = gw; i < st.m; i += nw) {
-    const T *a = entry_row<T>(p, w, slot_entry(st, p.idx, 0, static_cast<int>(i)), false);
+    const int e = slot_entry(st, p.idx, 0, static_cast<int>(i));
+    wait_row(p, e, st);
+    const T *a = entry_row<T>(p, w, e, false);
     float acc[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) acc[c] = 0.f;
     for (int k = lane; k < h; k += 32) {
-      const float av = to_f<T>(a[k]);
+      const float av = to_f<T>(__ldcg(a + k));
 #pragma unroll
       for (int c = 0; c < 16; ++c)
         if (c < C) acc[c] = fmaf(av, __ldg(W + c * h + k), acc[c]);
@@ -459,72 +505,72 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
     if (lane == 0) {
       float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
       for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
+      publish_row(p, st.out_row0 + static_cast<int>(i), h);
     }
   }
 }
 
-// bf16 variant (HBM-bound): W staged in shared memory as [h][C] fp32, each warp streams two rows
-// at a time with 16 B loads (lane owns 8-element chunks lane, lane+32, ...), h % 64 == 0.
-__device__ void simt_linear_out_bf16(const KParams &p, const DevStep &st, float *smem_w) {
-  const int h = p.hidden, C = st.gates;  // logits of this step (out_dim of its op type)
+// bf16 path output linear (HBM-bound): one warp, rows i0 and i0+1, W staged in shared memory as
+// [c][k] fp32 (or read from global when it does not fit); 16 B row loads (lane owns chunks lane,
+// lane+32, ...), h % 64 == 0.
+__device__ void linear_out_rows_bf16(const KParams &p, const DevStep &st, long i0, const float *Ws) {
+  const int h = p.hidden, C = st.gates;
   const DevWeightSet &w = p.w[st.wset];
-  const float *W = static_cast<const float *>(step_W(p, st));
   const float *bias = step_b(p, st);
-  for (int q = threadIdx.x; q < C * h; q += blockDim.x) smem_w[q] = W[q];  // [c][k]
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nch = h / 8;                 // 16 B chunks per row
   const int cpl = (nch + 31) / 32;       // chunks per lane (<= 4 for h <= 1024)
-  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
-  for (long i0 = gw * 2; i0 < st.m; i0 += nw * 2) {
-    uint4 v[2][4];
+  uint4 v[2][4];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const long i = i0 + r;
-      const __nv_bfloat16 *a = nullptr;
-      if (i < st.m) a = entry_row<__nv_bfloat16>(p, w, slot_entry(st, p.idx, 0, static_cast<int>(i)), false);
+  for (int r = 0; r < 2; ++r) {
+    const long i = i0 + r;
+    const __nv_bfloat16 *a = nullptr;
+    if (i < st.m) {
+      const int e = slot_entry(st, p.idx, 0, static_cast<int>(i));
+      wait_row(p, e, st);
+      a = entry_row<__nv_bfloat16>(p, w, e, false);
+    }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int ch = lane + 32 * q;
-        v[r][q] = (a != nullptr && q < cpl && ch < nch) ? __ldcg(reinterpret_cast<const uint4 *>(a) + ch)
-                                                         : make_uint4(0, 0, 0, 0);
+    for (int q = 0; q < 4; ++q) {
+      const int ch = lane + 32 * q;
+      v[r][q] = (a != nullptr && q < cpl && ch < nch) ? __ldcg(reinterpret_cast<const uint4 *>(a) + ch)
+                                                       : make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    float acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ch = lane + 32 * q;
+      if (q >= cpl || ch >= nch) continue;
+      const __nv_bfloat16 *e = reinterpret_cast<const __nv_bfloat16 *>(&v[r][q]);
+      float av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) av[u] = __bfloat162float(e[u]);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (c >= C) break;
+        const float4 w0 = *reinterpret_cast<const float4 *>(Ws + c * h + ch * 8);
+        const float4 w1 = *reinterpret_cast<const float4 *>(Ws + c * h + ch * 8 + 4);
+        acc[c] = fmaf(av[0], w0.x, fmaf(av[1], w0.y, fmaf(av[2], w0.z, fmaf(av[3], w0.w, acc[c]))));
+        acc[c] = fmaf(av[4], w1.x, fmaf(av[5], w1.y, fmaf(av[6], w1.z, fmaf(av[7], w1.w, acc[c]))));
       }
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      float acc[16];
+    for (int c = 0; c < 16; ++c) {
+      float x = acc[c];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int ch = lane + 32 * q;
-        if (q >= cpl || ch >= nch) continue;
-        const __nv_bfloat16 *e = reinterpret_cast<const __nv_bfloat16 *>(&v[r][q]);
-        float av[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) av[u] = __bfloat162float(e[u]);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          if (c >= C) break;
-          const float4 w0 = *reinterpret_cast<const float4 *>(smem_w + c * h + ch * 8);
-          const float4 w1 = *reinterpret_cast<const float4 *>(smem_w + c * h + ch * 8 + 4);
-          acc[c] = fmaf(av[0], w0.x, fmaf(av[1], w0.y, fmaf(av[2], w0.z, fmaf(av[3], w0.w, acc[c]))));
-          acc[c] = fmaf(av[4], w1.x, fmaf(av[5], w1.y, fmaf(av[6], w1.z, fmaf(av[7], w1.w, acc[c]))));
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        float x = acc[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        acc[c] = x;
-      }
-      const long i = i0 + r;
-      if (lane == 0 && i < st.m) {
-        float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-        for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
-      }
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      acc[c] = x;
+    }
+    const long i = i0 + r;
+    if (lane == 0 && i < st.m) {
+      float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
+      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
+      publish_row(p, st.out_row0 + static_cast<int>(i), h);
     }
   }
 }
@@ -549,15 +595,16 @@ __device__ void collect_roots(const KParams &p) {
 __global__ void __launch_bounds__(kThreads, 1) ed_persistent_f32(const __grid_constant__ KParams p) {
   unsigned int epoch = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[0] = globaltimer();
-  for (int s = 0; s < p.num_steps; ++s) {
+  for (int s = 0; s < p.num_steps; ++s) {  // dataflow: tasks wait on their input rows, no barrier
     const DevStep st = p.steps[s];
     if (st.cell == ED_CELL_LINEAR_OUT || st.cell == kCellTaggerOut)
       simt_linear_out<float>(p, st);
     else
       simt_gemm_step<float>(p, st);
-    grid_sync(p.bar, p.launch_id, epoch);
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[s + 1] = globaltimer();
+    __syncthreads();
+    if (threadIdx.x == 0) stamp_step(p, s);
   }
+  grid_sync(p.bar, p.launch_id, epoch);  // roots are read by any CTA
   collect_roots<float>(p);
 }
 
@@ -641,6 +688,10 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   if (valid && st.nslots > 1) e1 = slot_entry(st, p.idx, 1, i);
   if (e0 < 0) e0 = p.zero_row;  // external inputs have no c / h record here
   if (e1 < 0) e1 = p.zero_row;
+  if (valid && !(row_ready(p, e0, st) && row_ready(p, e1, st))) {  // acquire the rows read below
+    wait_row(p, e0, st);
+    wait_row(p, e1, st);
+  }
   const float4 *cp0 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e0) * h + jb);
   const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1) * h + jb);
   const __nv_bfloat16 *Hb = static_cast<const __nv_bfloat16 *>(p.H);
@@ -652,6 +703,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
     if (valid) {
       wbeg = __ldg(p.idx + st.var_off + i);
       wend = __ldg(p.idx + st.var_off + i + 1);
+      for (int w = wbeg; w < wend; ++w) wait_row(p, __ldg(p.idx + w), st);  // words ending here (c^w, l_w)
     }
   }
   float4 cn[NC > 0 ? 2 * NC : 1];
@@ -783,6 +835,22 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
     }
   }
+  if (valid) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // rows may be read by TMA (async proxy)
+    publish_row(p, static_cast<int>(orow), ngroups * 16);
+  }
+}
+
+// Work items of a step: tensor-core tiles (row tile x column tile), or SIMT groups of kSimtRows
+// rows.  Item t of step s runs on CTA (t + off_s) mod G, off_s = running item count mod G, so
+// consecutive (often independent) steps land on different SMs.
+constexpr int kSimtRows = 8;  // 4 epilogue warps x 2 rows
+__device__ __forceinline__ int step_items(const DevStep &st) {
+  if (is_umma_cell(st.cell)) return ((st.m + kTileM - 1) / kTileM) * st.n_col_tiles;
+  return (st.m + kSimtRows - 1) / kSimtRows;
+}
+__device__ __forceinline__ int first_item(uint32_t off) {
+  return static_cast<int>((blockIdx.x + gridDim.x - off % gridDim.x) % gridDim.x);
 }
 
 __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid_constant__ KParams p) {
@@ -790,8 +858,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stages = smem;
   const void **rowtab = reinterpret_cast<const void **>(smem + kStages * kStageBytes);  // [2][128][2] row ptrs
-  float *sbias = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + 2 * kRowTab + kBiasBytes);
+  float *sbias = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab + kEntTab);
+  float *swout = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes +
+                                                kWoutBytes);
   uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = bars + 2 * kStages + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);
 
@@ -815,222 +885,216 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  unsigned int epoch = 0;
-  Pipe pipe;
-  uint32_t tab_tile = 0;        // loader threads: row-table buffer toggle
-  uint32_t cp_pending = 0;      // cp.async warp: committed groups not yet released
-  bool tab_prebuilt = false;    // loader threads: next step's first row table already built
-  int b_pre = 0;                // B loader: stages of this step's first tile issued in advance
   if (blockIdx.x == 0 && tid == 0) p.ts[0] = globaltimer();
 
+  const int h = p.hidden;
+  const int G = static_cast<int>(gridDim.x);
+  Pipe pipe;
+  uint32_t tab_tile = 0;    // loader threads: row-table buffer toggle
+  uint32_t cp_pending = 0;  // loader warps: committed cp.async groups not yet released
+  uint32_t off = 0;         // running item offset (work rotation)
+
+  // Every warp role walks the steps in order; there is no grid barrier between steps (dataflow).
   for (int s = 0; s < p.num_steps; ++s) {
     const DevStep st = p.steps[s];
+    const int T = step_items(st);
+    const int t0 = first_item(off);
+    off = (off + static_cast<uint32_t>(T)) % static_cast<uint32_t>(G);
+    if (t0 >= T) continue;  // no work for this CTA in this step
     ED_TRACE(p, s, 0, tid == 0);
     if (!is_umma_cell(st.cell)) {
-      if (st.cell == ED_CELL_LINEAR_OUT || st.cell == kCellTaggerOut)
-        simt_linear_out_bf16(p, st, reinterpret_cast<float *>(stages));
-      else simt_gemm_step<__nv_bfloat16>(p, st);
-    } else {
-      const int h = p.hidden;
-      const int ncols = st.gates * st.units;
-      const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
-      const int mt = (st.m + kTileM - 1) / kTileM;
-      const int T = mt * st.n_col_tiles;
+      // ---------------- SIMT step (output linear / tagger output): epilogue warps ----------------
       if (warp < 4) {
-        // ---------------- epilogue warps ----------------
-        const float *bsrc = step_b(p, st);
-        for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
+        const int C = st.gates;
+        const bool in_smem = C * h * 4 <= kWoutBytes;
+        if (in_smem) {
+          const float *W = static_cast<const float *>(step_W(p, st));
+          for (int q = tid; q < C * h; q += kEpiThreads) swout[q] = W[q];
+        }
         asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
-        for (int t = blockIdx.x; t < T; t += gridDim.x) {
-          const uint32_t acc = pipe.ti & 1u;
-          const uint32_t tacc = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * 256u;
-          const int row_tile = t / st.n_col_tiles, col_tile = t % st.n_col_tiles;
-          const uint32_t par = (pipe.ti >> 1) & 1u;
-          switch (st.cell) {
-            case ED_CELL_TREELSTM_LEAF:
-              umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_TREELSTM_INTERNAL:
-              umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_TREEGRU_LEAF:
-              umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_TREEGRU_INTERNAL:
-              umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_TREEFC_INTERNAL:
-              umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_LSTM:
-              umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_LATTICE_CHAR:
-              umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case ED_CELL_LATTICE_WORD:
-              umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            case kCellLatticeLink:
-              umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-            default:
-              umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, sbias); break;
-          }
-          ED_TRACE(p, s, 5, tid == 0 && t == (int)blockIdx.x);
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // h rows are read by TMA in later steps
-          tc_fence_before();
-          mbar_arrive(tempty + acc);
-          ED_TRACE(p, s, 6, tid == 0 && t == (int)blockIdx.x);
-          ++pipe.ti;
+        const float *Ws = in_smem ? swout : static_cast<const float *>(step_W(p, st));
+        for (int t = t0; t < T; t += G) linear_out_rows_bf16(p, st, static_cast<long>(t) * kSimtRows + 2 * warp, Ws);
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
+        if (tid == 0) stamp_step(p, s);
+      }
+      continue;
+    }
+    const int ncols = st.gates * st.units;
+    const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
+    if (warp < 4) {
+      // ---------------- epilogue warps ----------------
+      const float *bsrc = step_b(p, st);
+      const bool bias_smem = st.gates * h * 4 <= kBiasBytes;
+      if (bias_smem)
+        for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
+      const float *bias = bias_smem ? sbias : bsrc;
+      for (int t = t0; t < T; t += G) {
+        const uint32_t acc = pipe.ti & 1u;
+        const uint32_t tacc = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * 256u;
+        const int row_tile = t / st.n_col_tiles, col_tile = t % st.n_col_tiles;
+        const uint32_t par = (pipe.ti >> 1) & 1u;
+        switch (st.cell) {
+          case ED_CELL_TREELSTM_LEAF:
+            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_TREELSTM_INTERNAL:
+            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_TREEGRU_LEAF:
+            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_TREEGRU_INTERNAL:
+            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_TREEFC_INTERNAL:
+            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_LSTM:
+            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_LATTICE_CHAR:
+            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case ED_CELL_LATTICE_WORD:
+            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case kCellLatticeLink:
+            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          default:
+            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
         }
-      } else if (warp == 4) {
-        // ---------------- MMA issuer ----------------
-        for (int t = blockIdx.x; t < T; t += gridDim.x) {
-          const uint32_t acc = pipe.ti & 1u;
-          const uint32_t idesc = idesc_bf16(st.gates * tile_units(st, h, t % st.n_col_tiles));
-          if (lane == 0) {
-            mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
+        ED_TRACE(p, s, 5, tid == 0 && t == t0);
+        tc_fence_before();
+        mbar_arrive(tempty + acc);
+        ++pipe.ti;
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");  // sbias reused by the next step
+      if (tid == 0) stamp_step(p, s);
+    } else if (warp == 4) {
+      // ---------------- MMA issuer ----------------
+      for (int t = t0; t < T; t += G) {
+        const uint32_t acc = pipe.ti & 1u;
+        const uint32_t idesc = idesc_bf16(st.gates * tile_units(st, h, t % st.n_col_tiles));
+        if (lane == 0) {
+          mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem_base + acc * 256u;
+          for (int kc = 0; kc < kc_total; ++kc) {
+            const uint32_t stg = pipe.it % kStages;
+            mbar_wait(full + stg, (pipe.it / kStages) & 1u);
             tc_fence_after();
-            const uint32_t d = tmem_base + acc * 256u;
-            for (int kc = 0; kc < kc_total; ++kc) {
-              const uint32_t stg = pipe.it % kStages;
-              mbar_wait(full + stg, (pipe.it / kStages) & 1u);
-              tc_fence_after();
-              ED_TRACE(p, s, 3, kc == 0 && t == (int)blockIdx.x);
-              ED_TRACE(p, s, 8 + (kc & 15), t == (int)blockIdx.x);
-              const uint32_t a_addr = smem_u32(stages + stg * kStageBytes);
-              const uint32_t b_addr = a_addr + kAStage;
-              const uint64_t ad = sw128_desc(a_addr), bd = sw128_desc(b_addr);
+            ED_TRACE(p, s, 3, kc == 0 && t == t0);
+            const uint32_t a_addr = smem_u32(stages + stg * kStageBytes);
+            const uint32_t b_addr = a_addr + kAStage;
+            const uint64_t ad = sw128_desc(a_addr), bd = sw128_desc(b_addr);
 #pragma unroll
-              for (int k = 0; k < kChunkK / 16; ++k)
-                tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc > 0 || k > 0) ? 1u : 0u);
-              tc_commit(empty + stg);
-              ++pipe.it;
-            }
-            tc_commit(tfull + acc);
-            ED_TRACE(p, s, 4, t == (int)blockIdx.x);
+            for (int k = 0; k < kChunkK / 16; ++k)
+              tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc > 0 || k > 0) ? 1u : 0u);
+            tc_commit(empty + stg);
+            ++pipe.it;
           }
-          ++pipe.ti;
+          tc_commit(tfull + acc);
+          ED_TRACE(p, s, 4, t == t0);
         }
-        pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
-      } else if (warp == 5) {
-        // ---------------- weight (B) loader ----------------
-        // Weights do not depend on earlier batches, so before the grid barrier of this step the
-        // first stages of the next step's first tile are already issued (b_pre of them).
-        const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
-        const size_t ntot = static_cast<size_t>(st.gates) * h;
-        for (int t = blockIdx.x; t < T; t += gridDim.x) {
-          const int col_tile = t % st.n_col_tiles;
-          if (lane == 0) {
-            for (int kc = (t == static_cast<int>(blockIdx.x) ? b_pre : 0); kc < kc_total; ++kc) {
-              const uint32_t stg = pipe.it % kStages;
-              mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
-              ED_TRACE(p, s, 24 + (kc & 15), t == (int)blockIdx.x);
-              const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
-              mbar_arrive_tx(full + stg, nb);
-              const uint8_t *src = Wp + ((static_cast<size_t>(kc) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-              bulk_g2s(stages + stg * kStageBytes + kAStage, src, nb, full + stg);
-              ++pipe.it;
-            }
-          }
-        }
-        b_pre = 0;
-        if (s + 1 < p.num_steps && lane == 0) {
-          const DevStep nx = p.steps[s + 1];
-          if (is_umma_cell(nx.cell) &&
-              static_cast<int>(blockIdx.x) < ((nx.m + kTileM - 1) / kTileM) * nx.n_col_tiles) {
-            const int nkc = (cell_segments_dev(nx.cell) * h) / kChunkK;
-            const int ct = static_cast<int>(blockIdx.x) % nx.n_col_tiles;
-            const uint8_t *Wn = static_cast<const uint8_t *>(step_W(p, nx));
-            const size_t nt = static_cast<size_t>(nx.gates) * h;
-            const uint32_t nb = static_cast<uint32_t>(nx.gates * tile_units(nx, h, ct)) * 128u;
-            for (int kc = 0; kc < min(kStages, nkc); ++kc) {
-              const uint32_t stg = pipe.it % kStages;
-              mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
-              mbar_arrive_tx(full + stg, nb);
-              const uint8_t *src =
-                  Wn + ((static_cast<size_t>(kc) * nt + static_cast<size_t>(ct) * nx.gates * nx.units) * 128);
-              bulk_g2s(stages + stg * kStageBytes + kAStage, src, nb, full + stg);
-              ++pipe.it;
-              ++b_pre;
-            }
-          }
-        }
-        pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
-        b_pre = __shfl_sync(0xffffffffu, b_pre, 0);
-      } else {
-        // ---------------- operand (A) loaders: warps 6-7 (64 threads) ----------------
-        // A CONTIG operand (layout plan made its rows adjacent and aligned) is one TMA 128-row box.
-        // A gathered operand is fetched with 16 B cp.async per (row, chunk) from a per-tile table of
-        // row pointers (H rows or embedding rows); measured on B200 this beats TMA tile::gather4 for
-        // 128 B rows.  Each stage is released to the MMA with a lag of kLag stages.
-        const int lt = tid - 192;  // 0 .. kLoaderThreads-1
-        const int nseg = cell_segments_dev(st.cell);
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // H rows of earlier steps: generic -> async proxy
-        for (int t = blockIdx.x; t < T; t += gridDim.x) {
-          const int row_tile = t / st.n_col_tiles;
-          const void **tab;
-          if (t == static_cast<int>(blockIdx.x) && tab_prebuilt) {
-            tab = rowtab + ((tab_tile - 1) & 1u) * (kTileM * 2);  // built before the last grid barrier
-          } else {
-            tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
-            ++tab_tile;
-            build_row_table(p, st, row_tile, nseg, lt, tab);
-            asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
-          }
-          if (lt == 0) ED_TRACE(p, s, 1, t == (int)blockIdx.x);
-          const int nrows = min(kTileM, st.m - row_tile * kTileM);
+        ++pipe.ti;
+      }
+      pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
+    } else if (warp == 5) {
+      // ---------------- weight (B) loader: runs ahead across steps (weights are static) -----------
+      const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
+      const size_t ntot = static_cast<size_t>(st.gates) * h;
+      for (int t = t0; t < T; t += G) {
+        const int col_tile = t % st.n_col_tiles;
+        if (lane == 0) {
           for (int kc = 0; kc < kc_total; ++kc) {
             const uint32_t stg = pipe.it % kStages;
             mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
-            const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
-            uint8_t *a_dst = stages + stg * kStageBytes;
-            int cbase = -1;
-            if (segment_contig(st, seg, &cbase)) {
-              if (lt == 0) {
-                mbar_arrive_tx(full + stg, kAStage);
-                tma_row_box(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
-              }
-            } else {
-              if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
-              const uint32_t a_base = smem_u32(a_dst);
-              for (int c = lt; c < nrows * 8; c += kLoaderThreads) {  // rows past m are not loaded
-                const int r = c >> 3, ch = c & 7;
-                const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
-                cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
-              }
-            }
-            cp_async_commit();
-            if (++cp_pending == kLag) {
-              cp_async_wait<kLag - 1>();
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(full + (pipe.it + 1 - kLag) % kStages);
-              --cp_pending;
-            }
+            const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
+            mbar_arrive_tx(full + stg, nb);
+            const uint8_t *src = Wp + ((static_cast<size_t>(kc) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
+            bulk_g2s(stages + stg * kStageBytes + kAStage, src, nb, full + stg);
             ++pipe.it;
           }
-          if (lt == 0) ED_TRACE(p, s, 2, t == (int)blockIdx.x);
         }
-        // the row table of the next step's first tile only reads the (static) step table: build it
-        // before the grid barrier
-        tab_prebuilt = false;
-        if (s + 1 < p.num_steps) {
-          const DevStep nx = p.steps[s + 1];
-          if (is_umma_cell(nx.cell) &&
-              static_cast<int>(blockIdx.x) < ((nx.m + kTileM - 1) / kTileM) * nx.n_col_tiles) {
-            const void **ntab = rowtab + (tab_tile & 1u) * (kTileM * 2);
-            ++tab_tile;
-            build_row_table(p, nx, static_cast<int>(blockIdx.x) / nx.n_col_tiles, cell_segments_dev(nx.cell), lt, ntab);
-            asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
-            tab_prebuilt = true;
+      }
+      pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
+    } else {
+      // ---------------- operand (A) loaders: warps 6-11 ----------------
+      // Per tile: row table (static) -> wait until every input row is published (acquire) ->
+      // CONTIG operand: one TMA 128-row box; gathered operand: 16 B cp.async per (row, chunk).
+      // Stages are released to the MMA with a lag of kLag groups and drained at the end of every
+      // tile (a later tile may wait for rows this CTA's epilogue still has to produce).
+      const int lt = tid - 192;  // 0 .. kLoaderThreads-1
+      const int nseg = cell_segments_dev(st.cell);
+      for (int t = t0; t < T; t += G) {
+        const int row_tile = t / st.n_col_tiles;
+        const void **tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
+        ++tab_tile;
+        int ent[2][2];  // this thread's input rows (at most 2 rows x 2 segments)
+        int nent = 0;
+        for (int r = lt; r < kTileM; r += kLoaderThreads, ++nent) {
+          const int i = row_tile * kTileM + r;
+          const int iv = i < st.m ? i : (st.m - 1);  // rows past m repeat the last valid row
+#pragma unroll
+          for (int sg = 0; sg < 2; ++sg) {
+            tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H;
+            ent[nent][sg] = sg < nseg ? segment_entry(p, st, sg, iv) : -1;
           }
         }
-        // drain: release every stage still pending in this step
+        // readiness of every input row, checked in parallel; block only on the rows still pending
+        // (nothing of this CTA is in flight here: every tile is drained at its end)
+        bool ok = true;
+        for (int q = 0; q < nent; ++q) ok = ok && row_ready(p, ent[q][0], st) && row_ready(p, ent[q][1], st);
+        int all_ok;
+        asm volatile("{\n\t.reg .pred pi, po;\n\tsetp.ne.s32 pi, %1, 0;\n\t"
+                     "bar.red.and.pred po, 1, %2, pi;\n\tselp.s32 %0, 1, 0, po;\n\t}"
+                     : "=r"(all_ok) : "r"(static_cast<int>(ok)), "n"(kLoaderThreads) : "memory");
+        if (!all_ok) {
+          for (int q = 0; q < nent; ++q) {
+            wait_row(p, ent[q][0], st);
+            wait_row(p, ent[q][1], st);
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA below
+        if (lt == 0) ED_TRACE(p, s, 1, t == t0);
+        const int nrows = min(kTileM, st.m - row_tile * kTileM);
+        for (int kc = 0; kc < kc_total; ++kc) {
+          const uint32_t stg = pipe.it % kStages;
+          mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+          const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
+          uint8_t *a_dst = stages + stg * kStageBytes;
+          int cbase = -1;
+          if (segment_contig(st, seg, &cbase)) {
+            if (lt == 0) {
+              mbar_arrive_tx(full + stg, kAStage);
+              tma_row_box(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
+            }
+          } else {
+            if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
+            const uint32_t a_base = smem_u32(a_dst);
+            for (int c = lt; c < nrows * 8; c += kLoaderThreads) {  // rows past m are not loaded
+              const int r = c >> 3, ch = c & 7;
+              const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
+              cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
+            }
+          }
+          cp_async_commit();
+          if (++cp_pending == kLag) {
+            cp_async_wait<kLag - 1>();
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full + (pipe.it + 1 - kLag) % kStages);
+            --cp_pending;
+          }
+          ++pipe.it;
+        }
+        // drain: the tile's last stages must reach the MMA now (its rows may be awaited by other
+        // CTAs, and this CTA's next tile may be many steps away)
         cp_async_wait<0>();
         fence_proxy_async_smem();
         __syncwarp();
         for (; cp_pending > 0; --cp_pending)
           if (lane == 0) mbar_arrive(full + (pipe.it - cp_pending) % kStages);
+        if (lt == 0) ED_TRACE(p, s, 2, t == t0);
       }
     }
-    ED_TRACE(p, s, 7, tid == 0);
-    grid_sync(p.bar, p.launch_id, epoch);
-    if (blockIdx.x == 0 && tid == 0) p.ts[s + 1] = globaltimer();
   }
+  unsigned int epoch = 0;
+  grid_sync(p.bar, p.launch_id, epoch);  // every row is final: collect the instance outputs
   collect_roots<__nv_bfloat16>(p);
   tc_fence_before();
   __syncthreads();

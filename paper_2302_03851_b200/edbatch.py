@@ -308,9 +308,13 @@ class Workspace:
         return self._view(i["off_x"], i["num_rows"] * i["hidden"], torch.float32).view(i["num_rows"], i["hidden"])
 
     def step_times_ns(self) -> np.ndarray:
+        """Per device step: time from the completion of all earlier steps to this step's completion
+        (stamps are per-step completion maxima; steps overlap in the dataflow kernel, so a step
+        finishing before an earlier one gets 0)."""
         i = self.plan_info
-        ts = self._view(i["off_ts"], i["num_steps"] + 1, torch.int64).cpu().numpy()
-        return np.diff(ts)
+        ts = self._view(i["off_ts"], i["num_steps"] + 1, torch.int64).cpu().numpy().astype(np.int64)
+        run = np.maximum.accumulate(ts)
+        return np.maximum(ts[1:] - run[:-1], 0)
 
 
 def ed_execute(plan: Plan, weights: DeviceWeights, workspace: Workspace, out_root: Optional[torch.Tensor] = None,
