@@ -17,12 +17,19 @@ from .graph import Merged
 
 
 def schedule_order_layout(m: Merged, sched) -> List[int]:
-    """ED_LAYOUT_SCHEDULE_ORDER: rows assigned batch after batch, members in ascending global
-    id inside a batch.  Every result operand is then one contiguous block (SURVEY A-9)."""
+    """ED_LAYOUT_SCHEDULE_ORDER: rows assigned batch after batch (every result operand is then one
+    contiguous block, SURVEY A-9); inside a batch, members ordered by the latest batch that
+    produces one of their node inputs (-1 if none), then by global id (reading L-1)."""
+    batch_of = {}
+    for b, (_, members) in enumerate(sched):
+        for v in members:
+            batch_of[v] = b
     row = [-1] * m.n
     r = 0
     for _, members in sched:
-        for v in sorted(members):
+        def key(v):
+            return (max([batch_of[u] for u in m.node_inputs(v)], default=-1), v)
+        for v in sorted(members, key=key):
             row[v] = r
             r += 1
     assert r == m.n

@@ -550,8 +550,27 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
     }
     if (pl->row_of_node.size() != static_cast<size_t>(pl->V)) { delete pl; return fail(ED_E_UNSUPPORTED, "PQ layout planner not available"); }
   } else {
+    // ED_LAYOUT_SCHEDULE_ORDER: batches in schedule order; inside a batch, members ordered by the
+    // latest batch producing one of their inputs, then by id, so that rows whose inputs are ready
+    // early share the early tiles (the dataflow kernel starts a tile when its input rows are ready)
     pl->row_of_node.assign(pl->V, -1);
-    for (size_t k = 0; k < pl->members.size(); ++k) pl->row_of_node[pl->members[k]] = static_cast<int32_t>(k);
+    std::vector<int32_t> bidx(pl->V, -1);
+    const int nbat = static_cast<int>(pl->batch_type.size());
+    for (int b = 0; b < nbat; ++b)
+      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) bidx[pl->members[k]] = b;
+    int32_t r = 0;
+    for (int b = 0; b < nbat; ++b) {
+      std::vector<std::pair<int32_t, int32_t>> key;
+      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) {
+        const int32_t v = pl->members[k];
+        int32_t last = -1;
+        for (int q = pl->in_off[v]; q < pl->in_off[v + 1]; ++q)
+          if (pl->in_idx[q] >= 0) last = std::max(last, bidx[pl->in_idx[q]]);
+        key.emplace_back(last, v);
+      }
+      std::sort(key.begin(), key.end());
+      for (const auto &kv : key) pl->row_of_node[kv.second] = r++;
+    }
   }
   const double t3 = now_us();
   st = lower(pl);

@@ -844,7 +844,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
 // Work items of a step: tensor-core tiles (row tile x column tile), or SIMT groups of kSimtRows
 // rows.  Item t of step s runs on CTA (t + off_s) mod G, off_s = running item count mod G, so
 // consecutive (often independent) steps land on different SMs.
-constexpr int kSimtRows = 8;  // 4 epilogue warps x 2 rows
+constexpr int kSimtRows = 2 * (kThreadsTC / 32);  // every warp of the CTA, 2 rows each
 __device__ __forceinline__ int step_items(const DevStep &st) {
   if (is_umma_cell(st.cell)) return ((st.m + kTileM - 1) / kTileM) * st.n_col_tiles;
   return (st.m + kSimtRows - 1) / kSimtRows;
@@ -903,20 +903,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     if (t0 >= T) continue;  // no work for this CTA in this step
     ED_TRACE(p, s, 0, tid == 0);
     if (!is_umma_cell(st.cell)) {
-      // ---------------- SIMT step (output linear / tagger output): epilogue warps ----------------
-      if (warp < 4) {
-        const int C = st.gates;
-        const bool in_smem = C * h * 4 <= kWoutBytes;
-        if (in_smem) {
-          const float *W = static_cast<const float *>(step_W(p, st));
-          for (int q = tid; q < C * h; q += kEpiThreads) swout[q] = W[q];
-        }
-        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
-        const float *Ws = in_smem ? swout : static_cast<const float *>(step_W(p, st));
-        for (int t = t0; t < T; t += G) linear_out_rows_bf16(p, st, static_cast<long>(t) * kSimtRows + 2 * warp, Ws);
-        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
-        if (tid == 0) stamp_step(p, s);
+      // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
+      const int C = st.gates;
+      const bool in_smem = C * h * 4 <= kWoutBytes;
+      if (in_smem) {
+        const float *W = static_cast<const float *>(step_W(p, st));
+        for (int q = tid; q < C * h; q += kThreadsTC) swout[q] = W[q];
       }
+      __syncthreads();
+      const float *Ws = in_smem ? swout : static_cast<const float *>(step_W(p, st));
+      for (int t = t0; t < T; t += G) linear_out_rows_bf16(p, st, static_cast<long>(t) * kSimtRows + 2 * warp, Ws);
+      __syncthreads();  // swout is reused by the next SIMT step
+      if (tid == 0) stamp_step(p, s);
       continue;
     }
     const int ncols = st.gates * st.units;
