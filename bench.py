@@ -32,7 +32,8 @@ METRICS = {"cfg3": METRIC,
            "cfg1": "instances/sec TreeLSTM h=32 (cfg1: 8 random trees, fp32) per step, whole job",
            "cfg2": "instances/sec BiLSTM-tagger h=256 (cfg2: 64 sequences, bf16) per step, whole job",
            "cfg5": "instances/sec LatticeLSTM h=256 (cfg5: 512 lattices, bf16) per step, whole job",
-           "cfg4_treefc": "instances/sec TreeFC h=512 (cfg4: 1024 trees, bf16) per step, whole job"}
+           "cfg4_treefc": "instances/sec TreeFC h=512 (cfg4: 1024 trees, bf16) per step, whole job",
+           "cfg4_mvrnn": "instances/sec MV-RNN h=512 (cfg4: 1024 trees, bf16) per step, whole job"}
 CONFIGS = {
     "cfg3": "cfg3 TreeLSTM h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16, FSM L>I>O",
     "cfg3_gru": "cfg3 TreeGRU h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
@@ -40,6 +41,7 @@ CONFIGS = {
     "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16, FSM F>B>T",
     "cfg5": "cfg5 LatticeLSTM h=256, 512 character lattices (chars U[10,50], word p=0.3), bf16",
     "cfg4_treefc": "cfg4 TreeFC h=512, 1024 random trees (leaves U[5,40]), bf16",
+    "cfg4_mvrnn": "cfg4 MV-RNN h=512, 1024 random trees (leaves U[5,40], 1024 word vectors + matrices), bf16",
 }
 
 
@@ -63,6 +65,8 @@ def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
         return W.lattice(512, (10, 50), 256, "bf16", 5 + 100 * rank)
     if name == "cfg4_treefc":
         return W.treefc(1024, (5, 40), 512, "bf16", 4 + 100 * rank)
+    if name == "cfg4_mvrnn":
+        return W.treefc(1024, (5, 40), 512, "bf16", 4 + 100 * rank, cell="mvrnn")
     raise KeyError(name)
 
 
@@ -89,6 +93,10 @@ def step_work(kind: str, m: int, h: int, C: int, elt: int):
         return 2 * m * (2 * h * 3 * h + 2 * h * h), m * (2 * elt * h + elt * h)
     if kind == "treefc_internal":
         return 2 * m * 2 * h * h, m * (2 * elt * h + elt * h)
+    if kind == "mvrnn_internal":
+        # p = tanh(W [B a; A b] + b): 2 matvecs (2h^2 each) + K=2h GEMM; P = W_M [A; B]: 4h^3.
+        # bytes: the two child matrices read once, P written, vectors
+        return m * (2 * 2 * h * h + 2 * 2 * h * h + 4 * h * h * h), m * (3 * elt * h * h + 3 * elt * h + 2 * elt * h)
     if kind == "lstm":
         return 2 * m * 2 * h * 4 * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h)
     if kind == "tagger":
@@ -107,6 +115,8 @@ def weight_bytes(kind: str, h: int, C: int, elt: int) -> int:
         return 4 * C * h
     if kind == "tagger":
         return elt * 2 * h * h + 4 * h + 4 * C * h + 4 * C
+    if kind == "mvrnn_internal":
+        return 2 * elt * 2 * h * h + 4 * h   # W and W_M (word vectors/matrices: per-node bytes)
     G, S = g[kind]
     return elt * G * h * S * h + 4 * G * h
 

@@ -143,6 +143,9 @@ typedef struct {
   int64_t y_cols;
   int64_t off_x;              /*   X [num_rows x hidden] f32 (lattice link gates)         */
   int64_t off_ts;             /*   u64 %globaltimer stamp after each device step (num_steps+1) */
+  int64_t off_u;              /*   U [num_rows x 2 hidden] (dtype): MV-RNN [B a; A b], or -1  */
+  int64_t off_m;              /*   Mx [num_rows x hidden x hidden] (dtype): MV-RNN node       */
+                              /*   matrices, each stored TRANSPOSED (row k = column k of P), or -1 */
   double plan_us;             /* host time spent in ed_plan                               */
   double schedule_us;
   double layout_us;
@@ -153,7 +156,10 @@ typedef struct {
  *   b     fp32 bias [G*h] (logical order)
  *   W2,b2 second matrix (TAGGER: [C, h]; LATTICE_WORD: link gate [h, 2h]; MVRNN: W_M [h, 2h])
  *   emb   embedding table [emb_rows, h] (dtype of the plan); emb2 second table (lattice chars)
- *   mat   MV-RNN word matrices [emb_rows, h, h] (dtype of the plan)                        */
+ *   mat   MV-RNN word matrices, packed by ed_pack_weights(ED_CELL_MVRNN_INTERNAL, h, emb_rows,
+ *         dtype, 2, ...) from the logical [emb_rows, h, h] table: each matrix transposed.
+ *   MV-RNN (Socher et al. 2012; Table 4): W = [h, 2h] and b = [h] of
+ *         p = tanh(W [B a; A b] + b); W2 = W_M [h, 2h] of P = W_M [A; B]; emb = word vectors. */
 typedef struct {
   const void *W;
   const float *b;
@@ -199,7 +205,8 @@ ed_status_t ed_plan_get_slot_modes(const ed_plan_t *plan, int32_t *modes);
 
 void ed_plan_destroy(ed_plan_t *plan);
 
-/* Bytes of the packed form of a logical matrix.  which = 0: main W; 1: W2. */
+/* Bytes of the packed form of a logical matrix.  which = 0: main W; 1: W2; 2 (MV-RNN only): the
+ * word-matrix table, logical [out_dim, h, h] (out_dim = number of words). */
 int64_t ed_packed_bytes(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which);
 
 /* Pack a logical fp32 matrix (device, row-major [rows, cols] as in DESIGN.md §5) into the

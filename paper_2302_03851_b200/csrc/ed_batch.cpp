@@ -137,13 +137,14 @@ struct ed_plan_s {
   std::vector<ed::DevStep> steps;
   std::vector<int32_t> idx;
   std::vector<int32_t> root_rows;
-  std::vector<int32_t> target;  // per row: h x device steps writing it (dataflow readiness)
+  std::vector<int32_t> target;  // per row: sum of ed::step_contrib over the device steps writing it
   int root_wset = 0;
   // workspace layout
   size_t off_bar = 0, off_ts = 0, off_steps = 0, off_idx = 0, off_roots = 0, off_target = 0, off_ready = 0,
-         off_h = 0, off_c = 0, off_y = 0, off_x = 0, ws_bytes = 0;
+         off_h = 0, off_c = 0, off_y = 0, off_x = 0, off_u = 0, off_m = 0, ws_bytes = 0;
   int64_t y_cols = 0;
   bool need_x = false;
+  bool need_mv = false;  // MV-RNN: U and Mx buffers
   // stats
   int64_t contig = 0, gather = 0, copy_bytes = 0, copy_kernels = 0;
   double plan_us = 0, sched_us = 0, layout_us = 0;
@@ -440,6 +441,40 @@ static ed_status_t lower(ed_plan_t *pl) {
       s2.arg[1] = st.out_row0;
       s2.nslots = 2;
       pl->steps.push_back(s2);
+    } else if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL) {
+      // step 1 (st): u = [B a; A b] (SIMT matvecs) -> U; step 2: p = tanh(W u + b) -> H, reading the
+      // node's own U rows; step 3: P^T = [A^T | B^T] W_M^T -> Mx (rows m*h, K = 2h, N = h)
+      pl->steps.back().units = 0;
+      pl->steps.back().n_col_tiles = 0;
+      ed::DevStep sp = st;
+      sp.cell = ed::kCellMvP;
+      sp.wsel = 0;
+      sp.gates = 1;
+      sp.units = ed::cell_units(sp.cell);
+      if (pl->dtype == ED_BF16) {
+        const int mt = (m + 127) / 128;
+        for (int u = sp.units; u >= 16; u -= 16)
+          if (mt * ((h + u - 1) / u) <= 148) sp.units = u;
+      }
+      sp.n_col_tiles = (h + sp.units - 1) / sp.units;
+      sp.mode[0] = 1;
+      sp.arg[0] = st.out_row0;
+      sp.mode[1] = 0;
+      sp.arg[1] = 0;
+      sp.nslots = 1;
+      pl->steps.push_back(sp);
+      ed::DevStep sm = st;
+      sm.cell = ed::kCellMvMat;
+      sm.wsel = 1;
+      sm.gates = 1;
+      sm.units = ed::cell_units(sm.cell);
+      if (pl->dtype == ED_BF16) {
+        const int64_t mt = (static_cast<int64_t>(m) * h + 127) / 128;
+        for (int u = sm.units; u >= 16; u -= 16)
+          if (mt * ((h + u - 1) / u) <= 148) sm.units = u;
+      }
+      sm.n_col_tiles = (h + sm.units - 1) / sm.units;
+      pl->steps.push_back(sm);
     } else if (ot.cell_kind == ED_CELL_TAGGER) {
       ed::DevStep s2 = st;  // y = W2 t + b2 with t in the node's own h row
       s2.cell = ed::kCellTaggerOut;
@@ -453,9 +488,16 @@ static ed_status_t lower(ed_plan_t *pl) {
       pl->steps.push_back(s2);
     }
   }
+  // readiness: target[row] = sum of what every device step writing the row publishes; a step that
+  // reads its own rows waits for what the earlier steps of its batch publish (self_need)
   pl->target.assign(V + 1, 0);
-  for (const auto &st : pl->steps)
-    for (int i = 0; i < st.m; ++i) pl->target[st.out_row0 + i] += h;
+  for (size_t k = 0; k < pl->steps.size(); ++k) {
+    ed::DevStep &st = pl->steps[k];
+    st.self_need = 0;
+    for (size_t q = k; q-- > 0 && pl->steps[q].out_row0 == st.out_row0 && pl->steps[q].m == st.m;)
+      st.self_need += ed::step_contrib(pl->steps[q].cell, h);
+    for (int i = 0; i < st.m; ++i) pl->target[st.out_row0 + i] += ed::step_contrib(st.cell, h);
+  }
   pl->root_rows.resize(pl->ninst);
   for (int i = 0; i < pl->ninst; ++i) {
     const int32_t r = pl->roots[i];
@@ -482,8 +524,13 @@ static ed_status_t lower(ed_plan_t *pl) {
       pl->y_cols = std::max<int64_t>(pl->y_cols, ot.out_dim);
     if (ot.cell_kind == ED_CELL_LATTICE_WORD) pl->need_x = true;
   }
+  pl->need_mv = false;
+  for (const auto &ot : pl->types)
+    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL) pl->need_mv = true;
   pl->off_y = off; off = align_up(off + 4 * rows * pl->y_cols, 1024);
   pl->off_x = off; if (pl->need_x) off = align_up(off + 4 * rows * h, 1024);
+  pl->off_u = off; if (pl->need_mv) off = align_up(off + elt * rows * 2 * h, 1024);
+  pl->off_m = off; if (pl->need_mv) off = align_up(off + elt * rows * h * h, 1024);
   pl->ws_bytes = off;
   // host blob mirrors [ts .. roots] so one async H2D uploads the static part
   pl->blob.assign(pl->off_ready - pl->off_ts, 0);
@@ -530,6 +577,9 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
     if (ot.weight_set < 0 || ot.weight_set >= ed::kMaxWeightSets) { delete pl; return fail(ED_E_TYPE, tag + ": weight_set out of range"); }
     if (ot.num_slots < 0 || ot.num_slots > 2) { delete pl; return fail(ED_E_TYPE, tag + ": num_slots must be 0..2"); }
     if ((ot.cell_kind == ED_CELL_LINEAR_OUT || ot.cell_kind == ED_CELL_TAGGER) && (ot.out_dim <= 0 || ot.out_dim > 16)) { delete pl; return fail(ED_E_TYPE, tag + ": out_dim must be 1..16"); }
+    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL && (ot.num_slots != 2 || ot.variadic || ot.has_ext)) { delete pl; return fail(ED_E_TYPE, tag + ": MV-RNN cells take exactly 2 fixed slots"); }
+    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL && ot.hidden % 8 != 0) { delete pl; return fail(ED_E_TYPE, tag + ": MV-RNN needs hidden % 8 == 0"); }
+    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL && ot.hidden > 2048) { delete pl; return fail(ED_E_UNSUPPORTED, tag + ": MV-RNN needs hidden <= 2048"); }
     if (ot.dtype == ED_BF16 && ot.hidden % 64 != 0) { delete pl; return fail(ED_E_TYPE, tag + ": bf16 path needs hidden % 64 == 0"); }
     if (!ed::cell_implemented(ot.cell_kind)) { delete pl; return fail(ED_E_UNSUPPORTED, tag + ": cell kind not implemented by this build"); }
   }
@@ -605,6 +655,8 @@ ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
   o->off_y = static_cast<int64_t>(pl->off_y);
   o->y_cols = pl->y_cols;
   o->off_x = pl->need_x ? static_cast<int64_t>(pl->off_x) : -1;
+  o->off_u = pl->need_mv ? static_cast<int64_t>(pl->off_u) : -1;
+  o->off_m = pl->need_mv ? static_cast<int64_t>(pl->off_m) : -1;
   o->off_ts = static_cast<int64_t>(pl->off_ts);
   o->plan_us = pl->plan_us;
   o->schedule_us = pl->sched_us;
@@ -692,6 +744,11 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
       if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_c + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
       if (ce == cudaSuccess && pl->need_x)
         ce = cudaMemsetAsync(base + pl->off_x + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
+      if (ce == cudaSuccess && pl->need_mv) {
+        const size_t hh = static_cast<size_t>(pl->hidden);
+        ce = cudaMemsetAsync(base + pl->off_u + elt * pl->V * 2 * hh, 0, elt * 2 * hh, s);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_m + elt * pl->V * hh * hh, 0, elt * hh * hh, s);
+      }
     }
     if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
     WsRegistry &reg = ws_registry();
@@ -711,6 +768,8 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   p.C = reinterpret_cast<float *>(base + pl->off_c);
   p.Y = reinterpret_cast<float *>(base + pl->off_y);
   p.X = pl->need_x ? reinterpret_cast<float *>(base + pl->off_x) : nullptr;
+  p.U = pl->need_mv ? base + pl->off_u : nullptr;
+  p.Mx = pl->need_mv ? base + pl->off_m : nullptr;
   p.bar = reinterpret_cast<unsigned int *>(base + pl->off_bar);
   p.ts = reinterpret_cast<unsigned long long *>(base + pl->off_ts);
   p.ready = reinterpret_cast<int *>(base + pl->off_ready);
@@ -735,14 +794,25 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
     const ed_weight_set_t &ws_ = w->sets[k];
     p.w[k] = ed::DevWeightSet{ws_.W, ws_.b, ws_.W2, ws_.b2, ws_.emb, ws_.emb2, ws_.mat, ws_.emb_rows, ws_.emb2_rows};
   }
+  for (const auto &ot : pl->types) {
+    const ed_weight_set_t &s_ = w->sets[ot.weight_set];
+    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL && (!s_.mat || s_.emb_rows <= 0 || !s_.emb || !s_.W || !s_.b || !s_.W2))
+      return fail(ED_E_INVALID_ARG, "MV-RNN weight set needs W, b, W2 (W_M), emb and mat with emb_rows > 0");
+  }
   if (pl->dtype == ED_BF16) {
-    if (!encode_rows(&p.tm_h1, p.H, pl->V + 1, pl->hidden, 1) ||
-        !encode_rows(&p.tm_h128, p.H, pl->V + 1, pl->hidden, 128))
+    const int64_t hh = pl->hidden;
+    if (!encode_rows(&p.tm_h128, p.H, pl->V + 1, hh, 128))
       return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for the H buffer");
-    for (int k = 0; k < w->num_sets; ++k)
-      if (w->sets[k].emb && w->sets[k].emb_rows > 0 &&
-          !encode_rows(&p.tm_emb1[k], w->sets[k].emb, w->sets[k].emb_rows, pl->hidden, 1))
-        return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for an embedding table");
+    if (pl->need_mv) {
+      if (!encode_rows(&p.tm_u, p.U, pl->V + 1, 2 * hh, 128) || !encode_rows(&p.tm_mx, p.Mx, (pl->V + 1) * hh, hh, 64))
+        return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for the MV-RNN buffers");
+      for (const auto &ot : pl->types) {
+        if (ot.cell_kind != ED_CELL_MVRNN_INTERNAL) continue;
+        const ed_weight_set_t &s_ = w->sets[ot.weight_set];
+        if (!encode_rows(&p.tm_mat[ot.weight_set], s_.mat, static_cast<int64_t>(s_.emb_rows) * hh, hh, 64))
+          return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for a word-matrix table");
+      }
+    }
   }
   e = ed::launch_persistent(p, pl->dtype, pl->grid, stream);
   if (e) return fail(ED_E_CUDA, std::string("launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));

@@ -13,6 +13,13 @@ constexpr int kMaxWeightSets = 8;
 // Device-only step kinds: the second contraction of a two-GEMM cell runs as its own step.
 constexpr int kCellLatticeLink = 101;  // l = s(W_l [x_e; c^w] + b_l) of LatticeLSTM word cells -> X
 constexpr int kCellTaggerOut = 102;    // y = W2 t + b2 of the BiLSTM tagger (t in the node's H row) -> Y
+// MV-RNN (Socher et al. 2012; Table 4) runs as three device steps over the same rows:
+//   ED_CELL_MVRNN_INTERNAL  u = [B a; A b]                         (matvecs, HBM-bound)    -> U
+//   kCellMvP                p = tanh(W u + b)                      (tensor cores, K = 2h)  -> H
+//   kCellMvMat              P^T = [A^T | B^T] W_M^T  (= (W_M [A;B])^T, tensor cores)       -> Mx
+// Node matrices are stored transposed (Mx row block of a node = M^T, row-major h x h).
+constexpr int kCellMvP = 103;
+constexpr int kCellMvMat = 104;
 constexpr int kMaxSlotsDev = 2;   // fixed slots the device reads (all cells have <= 2)
 
 // One batch of the schedule as the persistent kernel sees it (SoA-friendly 64 B record).
@@ -35,7 +42,8 @@ struct DevStep {
   int32_t gates;      // G: gate blocks of the main contraction
   int32_t nslots;     // fixed slots present
   int32_t wsel;       // 0: weight set W/b, 1: second matrix W2/b2
-  int32_t pad;
+  int32_t self_need;  // readiness a row of this step's own output block must reach before the step
+                      // may read it (= what earlier device steps of the same batch publish)
 };
 static_assert(sizeof(DevStep) == 64, "DevStep must be 64 bytes");
 
@@ -53,9 +61,10 @@ struct DevWeightSet {
 
 // Kernel parameters (passed as __grid_constant__ so the TMA descriptors below are addressable).
 struct alignas(64) KParams {
-  CUtensorMap tm_h1;                     // H rows, box {64 cols, 1 row}: gather4 / single rows
   CUtensorMap tm_h128;                   // H rows, box {64 cols, 128 rows}: contiguous blocks
-  CUtensorMap tm_emb1[kMaxWeightSets];   // embedding tables, box {64, 1}
+  CUtensorMap tm_u;                      // U rows (2h cols), box {64, 128}
+  CUtensorMap tm_mx;                     // node matrices Mx as [(rows * h) x h], box {64, 64}
+  CUtensorMap tm_mat[kMaxWeightSets];    // word-matrix tables as [(words * h) x h], box {64, 64}
   const DevStep *steps;
   const int32_t *idx;
   const int32_t *root_rows;   // per instance: row (>= 0) or external id (-1 - id)
@@ -63,12 +72,14 @@ struct alignas(64) KParams {
   float *C;                   // [rows x hidden]
   float *Y;                   // [rows x ycols]
   float *X;                   // [rows x hidden] (lattice link gates) or null
+  void *U;                    // [rows x 2 hidden] (MV-RNN matvec results [B a; A b]) or null
+  void *Mx;                   // [rows x hidden x hidden] (MV-RNN node matrices, transposed) or null
   unsigned int *bar;          // grid barrier counter (zeroed before launch)
   unsigned long long *ts;     // [num_steps + 1]
   void *out_root;             // [num_inst x hidden] or null
   unsigned long long *trace;  // [num_steps x 64] phase stamps of CTA 0, or null
   int *ready;                 // [rows] hidden units published per row (zeroed every launch)
-  const int *target;          // [rows] units a row holds when final (h x device steps writing it)
+  const int *target;          // [rows] units a row holds when final (sum of step_contrib)
   int32_t num_steps;
   int32_t hidden;
   int32_t rows;
@@ -95,6 +106,8 @@ inline int cell_gates(int cell) {
     case ED_CELL_TAGGER: return 1;
     case ED_CELL_MVRNN_INTERNAL: return 1;
     case kCellLatticeLink: return 1;
+    case kCellMvP: return 1;
+    case kCellMvMat: return 1;
     default: return 0;
   }
 }
@@ -114,6 +127,8 @@ inline int cell_units(int cell) {
     case ED_CELL_LATTICE_WORD: return 80;       // N = 240
     case kCellLatticeLink: return 256;          // N = 256
     case ED_CELL_TAGGER: return 256;            // N = 256
+    case kCellMvP: return 256;                  // N = 256
+    case kCellMvMat: return 256;                // N = 256 (columns of P^T)
     default: return 0;
   }
 }
@@ -130,7 +145,8 @@ inline bool cell_implemented(int cell) {
     case ED_CELL_LSTM:
     case ED_CELL_TAGGER:
     case ED_CELL_LATTICE_CHAR:
-    case ED_CELL_LATTICE_WORD: return true;
+    case ED_CELL_LATTICE_WORD:
+    case ED_CELL_MVRNN_INTERNAL: return true;
     default: return false;
   }
 }
@@ -144,6 +160,10 @@ inline int cell_segments(int cell) {
     default: return 2;
   }
 }
+
+// Readiness units a device step publishes per row of its output block when it completes: h for
+// row-vector results; h * h (elements) for the MV-RNN matrix product.
+inline int step_contrib(int cell, int h) { return cell == kCellMvMat ? h * h : h; }
 
 // Launch entry points implemented in ed_kernels.cu (return cudaError_t as int).
 int launch_persistent(const KParams &p, int dtype, int grid, void *stream);

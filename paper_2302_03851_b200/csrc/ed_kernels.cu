@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "ed_internal.h"
 
@@ -202,8 +203,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 // ---- dataflow readiness (replaces per-batch grid barriers) ----
-// ready[row] counts hidden units written to the row by finished device steps; target[row] = h x the
-// number of device steps that write it.  A consumer acquires ready[row] >= target[row] before reading
+// ready[row] counts units written to the row by finished device steps; target[row] = the sum of
+// step_contrib over the device steps that write it (h per row-vector result, h*h for a matrix).  A consumer acquires ready[row] >= target[row] before reading
 // the row; a producer publishes with a release-add after its stores.  Rows are only produced by
 // earlier device steps and every warp walks the steps in order, so waiting cannot deadlock.
 __device__ __forceinline__ int ld_acquire_s32(const int *a) {
@@ -212,15 +213,19 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
   return v;
 }
 // A step that reads its own rows (the second contraction of a two-GEMM cell: link gate, tagger
-// output) needs only the units of the earlier writer: target - h.
+// output, MV-RNN p) needs only what the earlier steps of its batch publish: st.self_need.
 __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep &st) {
   if (e < 0 || e >= p.rows) return;  // external rows are static
   int need = __ldg(p.target + e);
-  if (e >= st.out_row0 && e < st.out_row0 + st.m) need -= p.hidden;
+  if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
   if (need <= 0) return;
   unsigned spins = 0;
   while (ld_acquire_s32(p.ready + e) < need) {
-    if (++spins > (1u << 26)) __trap();  // watchdog
+    if (++spins > (1u << 26)) {  // watchdog: report the stuck dependency, then abort the launch
+      printf("ed_batch watchdog: block %d thread %d cell %d out_row0 %d row %d ready %d need %d\n", blockIdx.x,
+             threadIdx.x, st.cell, st.out_row0, e, ld_acquire_s32(p.ready + e), need);
+      __trap();
+    }
     __nanosleep(32);
   }
 }
@@ -228,7 +233,7 @@ __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep 
 __device__ __forceinline__ bool row_ready(const KParams &p, int e, const DevStep &st) {
   if (e < 0 || e >= p.rows) return true;
   int need = __ldg(p.target + e);
-  if (e >= st.out_row0 && e < st.out_row0 + st.m) need -= p.hidden;
+  if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
   return need <= 0 || ld_acquire_s32(p.ready + e) >= need;
 }
 __device__ __forceinline__ void publish_row(const KParams &p, int row, int units) {
@@ -313,6 +318,8 @@ __device__ __forceinline__ const T *segment_row(const KParams &p, const DevStep 
     }
     return entry_row<T>(p, w, slot_entry(st, p.idx, 0, i), false);
   }
+  // MV-RNN p step: K segment s of u = [B a; A b] in the node's own U row
+  if (cell == kCellMvP) return static_cast<const T *>(p.U) + (static_cast<size_t>(st.out_row0 + i) * 2 + s) * p.hidden;
   // lattice link gate: x_e of the word's end char comes from the char table (emb2)
   return entry_row<T>(p, w, slot_entry(st, p.idx, s, i), cell == kCellLatticeLink && s == 0);
 }
@@ -323,6 +330,7 @@ __device__ __forceinline__ bool ext_first_cell(int cell) {
 }
 // Operand entry of K segment s for member i: >= 0 row of H; < 0 embedding row (-1 - id).
 __device__ __forceinline__ int segment_entry(const KParams &p, const DevStep &st, int s, int i) {
+  if (st.cell == kCellMvP) return st.out_row0 + i;  // own U row (published by the matvec step)
   if (ext_first_cell(st.cell)) {
     if (s == 0) return -1 - __ldg(p.idx + st.ext_off + i);
     return slot_entry(st, p.idx, 0, i);
@@ -331,6 +339,10 @@ __device__ __forceinline__ int segment_entry(const KParams &p, const DevStep &st
 }
 // Whether K segment s is one contiguous block of H rows (layout plan made it adjacent + aligned).
 __device__ __forceinline__ bool segment_contig(const DevStep &st, int s, int *base) {
+  if (st.cell == kCellMvP) {  // the node's own U rows: always one block
+    *base = st.out_row0;
+    return true;
+  }
   int slot = s;
   if (ext_first_cell(st.cell)) {
     if (s == 0) return false;
@@ -379,6 +391,7 @@ __device__ __forceinline__ void cell_epilogue(const KParams &p, const DevStep &s
       break;
     }
     case ED_CELL_TREEFC_INTERNAL:
+    case kCellMvP:  // MV-RNN p = tanh(W [B a; A b] + b)
       hv = act_tanh<T>(z[0]);
       has_c = false;
       break;
@@ -575,6 +588,127 @@ __device__ void linear_out_rows_bf16(const KParams &p, const DevStep &st, long i
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// MV-RNN (Socher et al. 2012; Table 4).  Node matrices are stored transposed: the Mx
+// block of a node (and every word matrix of the packed table) holds M^T, row-major h x h.
+// ------------------------------------------------------------------------------------------------
+// Matrix of operand entry e: a node record (Mx) or a word matrix of the packed table.
+template <typename T>
+__device__ __forceinline__ const T *mv_matrix(const KParams &p, const DevStep &st, int e) {
+  const size_t hh = static_cast<size_t>(p.hidden) * p.hidden;
+  return e >= 0 ? static_cast<const T *>(p.Mx) + static_cast<size_t>(e) * hh
+                : static_cast<const T *>(p.w[st.wset].mat) + static_cast<size_t>(-1 - e) * hh;
+}
+
+// Matvec step u = [B a; A b] -> U (HBM-bound: every item streams one h x h matrix once).
+// Item t (one CTA): member i = t / 2, half q = t % 2; q = 0: B a (matrix of slot 1, vector of slot
+// 0) -> U[:, 0:h]; q = 1: A b -> U[:, h:2h].  (M x)[c] = sum_k M^T[k][c] x[k]: thread (rg, cg) owns
+// VEC columns and a strided set of rows k; partial sums are reduced through shared memory.
+// svec: h floats; sred: blockDim.x * VEC floats.
+template <typename T>
+__device__ void mv_vec_items(const KParams &p, const DevStep &st, int t_begin, int t_step, float *svec, float *sred) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int h = p.hidden, nthr = blockDim.x, tid = threadIdx.x;
+  const int ncg = h / VEC;
+  const int nrg = ncg <= nthr ? nthr / ncg : 1;
+  const int T_ = 2 * st.m;
+  T *U = static_cast<T *>(p.U);
+  for (int t = t_begin; t < T_; t += t_step) {
+    const int i = t >> 1, q = t & 1;
+    const int ev = slot_entry(st, p.idx, q, i);      // vector: a (q = 0) or b (q = 1)
+    const int em = slot_entry(st, p.idx, 1 - q, i);  // matrix: B (q = 0) or A (q = 1)
+    wait_row(p, ev, st);
+    wait_row(p, em, st);
+    const T *vec = entry_row<T>(p, p.w[st.wset], ev, false);
+    const T *Mt = mv_matrix<T>(p, st, em);
+    for (int k = tid; k < h; k += nthr) svec[k] = to_f<T>(__ldcg(vec + k));
+    __syncthreads();
+    T *dst = U + (static_cast<size_t>(st.out_row0 + i) * 2 + q) * h;
+    for (int cg0 = 0; cg0 < ncg; cg0 += nthr) {  // one pass unless h > nthr * VEC
+      const int rg = ncg <= nthr ? tid / ncg : 0;
+      const int cg = ncg <= nthr ? tid % ncg : cg0 + tid;
+      float acc[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+      if (rg < nrg && cg < ncg) {
+        const uint4 *col = reinterpret_cast<const uint4 *>(Mt + static_cast<size_t>(cg) * VEC);
+        const size_t ld = static_cast<size_t>(h) / VEC;  // uint4 per matrix row
+        int k = rg;
+        for (; k + 3 * nrg < h; k += 4 * nrg) {
+          uint4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldcg(col + static_cast<size_t>(k + u * nrg) * ld);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const T *e = reinterpret_cast<const T *>(&v[u]);
+            const float x = svec[k + u * nrg];
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) acc[c] = fmaf(to_f<T>(e[c]), x, acc[c]);
+          }
+        }
+        for (; k < h; k += nrg) {
+          const uint4 v = __ldcg(col + static_cast<size_t>(k) * ld);
+          const T *e = reinterpret_cast<const T *>(&v);
+          const float x = svec[k];
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) acc[c] = fmaf(to_f<T>(e[c]), x, acc[c]);
+        }
+      }
+      if (nrg == 1) {
+        if (cg < ncg)
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) dst[cg * VEC + c] = from_f<T>(acc[c]);
+      } else {
+        if (rg < nrg)
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) sred[rg * h + cg * VEC + c] = acc[c];
+        __syncthreads();
+        for (int c = tid; c < h; c += nthr) {
+          float sum = 0.f;
+          for (int r = 0; r < nrg; ++r) sum += sred[r * h + c];
+          dst[c] = from_f<T>(sum);
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // U is read by TMA in the p step
+    __threadfence();
+    __syncthreads();  // svec / sred reused; every store of the item precedes the publication
+    if (tid == 0) publish_row(p, st.out_row0 + i, h / 2);
+  }
+}
+
+// fp32 path of the matrix product: P^T[r][j] = sum_k [A^T | B^T][r][k] W_M[j][k] (Wt = W_M^T
+// [2h][h]); warp task = (matrix row R of the batch's m * h rows, 32 columns).
+template <typename T>
+__device__ void simt_mv_mat(const KParams &p, const DevStep &st) {
+  const int h = p.hidden;
+  const T *Wt = static_cast<const T *>(step_W(p, st));
+  const int lane = threadIdx.x & 31;
+  const int nub = (h + 31) / 32;
+  const long tasks = static_cast<long>(st.m) * h * nub;
+  const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  T *Mx = static_cast<T *>(p.Mx);
+  for (long task = gw; task < tasks; task += nw) {
+    const long R = task / nub;
+    const int i = static_cast<int>(R / h), r = static_cast<int>(R % h);
+    const int j = static_cast<int>(task % nub) * 32 + lane;
+    const int e0 = slot_entry(st, p.idx, 0, i), e1 = slot_entry(st, p.idx, 1, i);
+    wait_row(p, e0, st);
+    wait_row(p, e1, st);
+    const int jj = j < h ? j : 0;
+    float z = 0.f;
+    for (int sg = 0; sg < 2; ++sg) {
+      const T *a = mv_matrix<T>(p, st, sg == 0 ? e0 : e1) + static_cast<size_t>(r) * h;
+      const T *wk = Wt + static_cast<size_t>(sg) * h * h + jj;
+      for (int k = 0; k < h; ++k) z = fmaf(to_f<T>(__ldcg(a + k)), to_f<T>(wk[static_cast<size_t>(k) * h]), z);
+    }
+    if (j < h) Mx[(static_cast<size_t>(st.out_row0 + i) * h + r) * h + j] = from_f<T>(z);
+    __syncwarp();
+    if (lane == 0) publish_row(p, st.out_row0 + i, min(32, h - (j - lane)));
+  }
+}
+
 template <typename T>
 __device__ void collect_roots(const KParams &p) {
   if (p.out_root == nullptr) return;
@@ -593,12 +727,18 @@ __device__ void collect_roots(const KParams &p) {
 // fp32 persistent kernel: all SIMT
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1) ed_persistent_f32(const __grid_constant__ KParams p) {
+  __shared__ float s_vec[2048];          // MV-RNN matvec operand (h <= 2048)
+  __shared__ float s_red[kThreads * 4];  // MV-RNN partial sums
   unsigned int epoch = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[0] = globaltimer();
   for (int s = 0; s < p.num_steps; ++s) {  // dataflow: tasks wait on their input rows, no barrier
     const DevStep st = p.steps[s];
     if (st.cell == ED_CELL_LINEAR_OUT || st.cell == kCellTaggerOut)
       simt_linear_out<float>(p, st);
+    else if (st.cell == ED_CELL_MVRNN_INTERNAL)
+      mv_vec_items<float>(p, st, blockIdx.x, gridDim.x, s_vec, s_red);
+    else if (st.cell == kCellMvMat)
+      simt_mv_mat<float>(p, st);
     else
       simt_gemm_step<float>(p, st);
     __syncthreads();
@@ -620,7 +760,7 @@ __device__ __forceinline__ bool is_umma_cell(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
          cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == kCellLatticeLink ||
-         cell == ED_CELL_TAGGER;
+         cell == ED_CELL_TAGGER || cell == kCellMvP || cell == kCellMvMat;
 }
 
 // Per-cell configuration of the tensor-core epilogue: G gates, U units per column tile (must
@@ -639,6 +779,7 @@ template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U
 template <> struct CellCfg<ED_CELL_LATTICE_WORD> { static constexpr int G = 3, U = 80, NC = 1, NH = 0; };
 template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
+template <> struct CellCfg<kCellMvP> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 
 // Row pointers (per K segment) of the 128 rows of a row tile; rows past m repeat the last valid row.
 __device__ __forceinline__ void build_row_table(const KParams &p, const DevStep &st, int row_tile, int nseg, int lt,
@@ -746,7 +887,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       z[g][4] += b1.x; z[g][5] += b1.y; z[g][6] += b1.z; z[g][7] += b1.w;
     }
     constexpr bool HAS_C = !(CELL == ED_CELL_TREEGRU_LEAF || CELL == ED_CELL_TREEGRU_INTERNAL ||
-                             CELL == ED_CELL_TREEFC_INTERNAL || CELL == ED_CELL_TAGGER);
+                             CELL == ED_CELL_TREEFC_INTERNAL || CELL == ED_CELL_TAGGER || CELL == kCellMvP);
     constexpr bool HAS_H = CELL != kCellLatticeLink;
     float hv[8] = {}, cv[8] = {};
     float hl[8], hr[8];
@@ -814,7 +955,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
           hv[k] = cv[k];
         } else if constexpr (CELL == kCellLatticeLink) {  // l = s(.) -> X
           cv[k] = sigm_fast(z[0][k]);
-        } else {  // tagger hidden: t = tanh(.) -> H
+        } else {  // tagger hidden t = tanh(.), MV-RNN p = tanh(.) -> H
           hv[k] = tanh_fast(z[0][k]);
         }
       }
@@ -841,11 +982,52 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   }
 }
 
+// Epilogue of one 128 x units tile of the MV-RNN matrix product: rows R = row_tile * 128 + r of the
+// batch's m * h rows of P^T (node i = R / h, matrix row R % h), stored bf16 into the node's Mx block.
+// A warp's 32 rows belong to one node (h % 64 == 0): lane 0 publishes 32 x units elements.
+__device__ __forceinline__ void mv_mat_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
+                                                uint32_t parity, int row_tile, int col_tile, int r) {
+  const int h = p.hidden;
+  const long R = static_cast<long>(row_tile) * kTileM + r;
+  const bool valid = R < static_cast<long>(st.m) * h;
+  const int i = valid ? static_cast<int>(R / h) : 0, rr = static_cast<int>(R % h);
+  const int jb = col_tile * st.units, cols = tile_units(st, h, col_tile);
+  __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(p.Mx) + (static_cast<size_t>(st.out_row0 + i) * h + rr) * h + jb;
+  mbar_wait(tfull_bar, parity);
+  tc_fence_after();
+#pragma unroll 1
+  for (int c0 = 0; c0 < cols; c0 += 32) {
+    float v[32];
+    tmem_ld16(tacc + static_cast<uint32_t>(c0), v);
+    if (c0 + 16 < cols) tmem_ld16(tacc + static_cast<uint32_t>(c0 + 16), v + 16);
+    tmem_wait_ld();
+    if (!valid) continue;
+    const int nc = min(32, cols - c0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q * 8 >= nc) break;
+      uint32_t pk[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(v[q * 8 + 2 * k], v[q * 8 + 2 * k + 1]);
+        pk[k] = *reinterpret_cast<uint32_t *>(&t);
+      }
+      *reinterpret_cast<uint4 *>(dst + c0 + q * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // Mx blocks are read by TMA later
+  __threadfence();
+  __syncwarp();
+  if (valid && (threadIdx.x & 31) == 0) publish_row(p, st.out_row0 + i, 32 * cols);
+}
+
 // Work items of a step: tensor-core tiles (row tile x column tile), or SIMT groups of kSimtRows
 // rows.  Item t of step s runs on CTA (t + off_s) mod G, off_s = running item count mod G, so
 // consecutive (often independent) steps land on different SMs.
 constexpr int kSimtRows = 2 * (kThreadsTC / 32);  // every warp of the CTA, 2 rows each
-__device__ __forceinline__ int step_items(const DevStep &st) {
+__device__ __forceinline__ int step_items(const DevStep &st, int h) {
+  if (st.cell == kCellMvMat) return static_cast<int>((static_cast<long>(st.m) * h + kTileM - 1) / kTileM) * st.n_col_tiles;
+  if (st.cell == ED_CELL_MVRNN_INTERNAL) return 2 * st.m;  // matvec: one CTA per (member, half)
   if (is_umma_cell(st.cell)) return ((st.m + kTileM - 1) / kTileM) * st.n_col_tiles;
   return (st.m + kSimtRows - 1) / kSimtRows;
 }
@@ -897,12 +1079,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   // Every warp role walks the steps in order; there is no grid barrier between steps (dataflow).
   for (int s = 0; s < p.num_steps; ++s) {
     const DevStep st = p.steps[s];
-    const int T = step_items(st);
+    const int T = step_items(st, h);
     const int t0 = first_item(off);
     off = (off + static_cast<uint32_t>(T)) % static_cast<uint32_t>(G);
     if (t0 >= T) continue;  // no work for this CTA in this step
     ED_TRACE(p, s, 0, tid == 0);
     if (!is_umma_cell(st.cell)) {
+      if (st.cell == ED_CELL_MVRNN_INTERNAL) {  // ---- MV-RNN matvecs: one CTA per item ----
+        __syncthreads();  // sbias / swout are free (previous step's epilogue done)
+        mv_vec_items<__nv_bfloat16>(p, st, t0, G, sbias, swout);
+        if (tid == 0) stamp_step(p, s);
+        continue;
+      }
       // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
       const int C = st.gates;
       const bool in_smem = C * h * 4 <= kWoutBytes;
@@ -922,7 +1110,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     if (warp < 4) {
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
-      const bool bias_smem = st.gates * h * 4 <= kBiasBytes;
+      const bool bias_smem = bsrc != nullptr && st.gates * h * 4 <= kBiasBytes;
       if (bias_smem)
         for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
       asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
@@ -951,6 +1139,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
           case kCellLatticeLink:
             umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case kCellMvP:
+            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+          case kCellMvMat:
+            mv_mat_epilogue(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid); break;
           default:
             umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
         }
@@ -1017,6 +1209,53 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // tile (a later tile may wait for rows this CTA's epilogue still has to produce).
       const int lt = tid - 192;  // 0 .. kLoaderThreads-1
       const int nseg = cell_segments_dev(st.cell);
+      if (st.cell == kCellMvMat) {
+        // MV-RNN matrix product: A rows = [A^T | B^T] rows of the children's matrices; each 64-row
+        // half of a tile lies in one node's block -> two TMA boxes {64 cols, 64 rows} per stage,
+        // from Mx (child node) or the packed word-matrix table (leaf).  No cp.async: stages are
+        // released right after issue.
+        const long mrows = static_cast<long>(st.m) * h;
+        for (int t = t0; t < T; t += G) {
+          const long R0 = static_cast<long>(t / st.n_col_tiles) * kTileM;
+          int ent[2][2], rr0[2], nh = 0;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const long R = R0 + q * 64;
+            if (R < mrows) {
+              const int node = static_cast<int>(R / h);
+              rr0[q] = static_cast<int>(R % h);
+              ent[q][0] = slot_entry(st, p.idx, 0, node);
+              ent[q][1] = slot_entry(st, p.idx, 1, node);
+              nh = q + 1;
+            }
+          }
+          for (int q = 0; q < nh; ++q) {
+            wait_row(p, ent[q][0], st);
+            wait_row(p, ent[q][1], st);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          for (int kc = 0; kc < kc_total; ++kc) {
+            const uint32_t stg = pipe.it % kStages;
+            mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+            const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
+            uint8_t *a_dst = stages + stg * kStageBytes;
+            if (lt == 0) {
+              mbar_arrive_tx(full + stg, static_cast<uint32_t>(nh) * 8192u);
+              for (int q = 0; q < nh; ++q) {
+                const int e = ent[q][seg];
+                if (e >= 0)
+                  tma_row_box(a_dst + q * 8192, &p.tm_mx, col0, e * h + rr0[q], full + stg);
+                else
+                  tma_row_box(a_dst + q * 8192, &p.tm_mat[st.wset], col0, (-1 - e) * h + rr0[q], full + stg);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full + stg);
+            ++pipe.it;
+          }
+        }
+        continue;
+      }
       for (int t = t0; t < T; t += G) {
         const int row_tile = t / st.n_col_tiles;
         const void **tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
@@ -1059,7 +1298,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           if (segment_contig(st, seg, &cbase)) {
             if (lt == 0) {
               mbar_arrive_tx(full + stg, kAStage);
-              tma_row_box(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
+              if (st.cell == kCellMvP)  // U rows: [B a | A b], 2h columns
+                tma_row_box(a_dst, &p.tm_u, seg * h + col0, cbase + row_tile * kTileM, full + stg);
+              else
+                tma_row_box(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
             }
           } else {
             if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
@@ -1144,12 +1386,30 @@ __global__ void copy_f32_kernel(const float *src, float *dst, long n) {
 static bool umma_cell_host(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
-         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == ED_CELL_TAGGER;
+         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == ED_CELL_TAGGER ||
+         cell == ED_CELL_MVRNN_INTERNAL;
+}
+
+// MV-RNN word-matrix table: dst[w][k][i] = src[w][i][k] (each matrix transposed), element type T.
+template <typename T>
+__global__ void pack_mat_transpose_kernel(const float *src, T *dst, long words, int h) {
+  const long hh = static_cast<long>(h) * h;
+  const long total = words * hh;
+  for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long w = q / hh;
+    const int k = static_cast<int>((q % hh) / h), i = static_cast<int>(q % h);
+    dst[q] = from_f<T>(src[w * hh + static_cast<long>(i) * h + k]);
+  }
 }
 
 // Logical shape of a cell's matrices (rows, cols).
 static void logical_shape(int cell, int h, int out_dim, int which, long *rows, long *cols) {
   if (cell == ED_CELL_LINEAR_OUT) { *rows = out_dim; *cols = h; return; }
+  if (which == 2) {  // MV-RNN word-matrix table [out_dim words][h][h]
+    if (cell != ED_CELL_MVRNN_INTERNAL) { *rows = 0; *cols = 0; return; }
+    *rows = static_cast<long>(out_dim) * h; *cols = h; return;
+  }
   if (which == 1) {
     if (cell == ED_CELL_TAGGER) { *rows = out_dim; *cols = h; return; }
     *rows = h; *cols = 2 * h; return;   // lattice link gate W_l, MV-RNN W_M
@@ -1173,10 +1433,16 @@ int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const f
   const int threads = 256;
   const long total = rows * cols;
   const int blocks = static_cast<int>((total + threads - 1) / threads < 4096 ? (total + threads - 1) / threads : 4096);
-  if (total == 0) return 0;
-  if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) {
+  if (total == 0) return which == 2 && cell != ED_CELL_MVRNN_INTERNAL ? static_cast<int>(cudaErrorInvalidValue) : 0;
+  if (which == 2) {
+    if (dtype == ED_BF16)
+      pack_mat_transpose_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), out_dim, hidden);
+    else
+      pack_mat_transpose_kernel<float><<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), out_dim, hidden);
+  } else if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) {
     copy_f32_kernel<<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), total);
-  } else if (dtype == ED_BF16 && umma_cell_host(cell) && (which == 0 || cell == ED_CELL_LATTICE_WORD)) {
+  } else if (dtype == ED_BF16 && umma_cell_host(cell) &&
+             (which == 0 || cell == ED_CELL_LATTICE_WORD || cell == ED_CELL_MVRNN_INTERNAL)) {
     if (hidden % 64 != 0) return static_cast<int>(cudaErrorInvalidValue);
     const int G = which == 0 ? cell_gates(cell) : 1;  // link gate W_l: one gate block
     pack_umma_kernel<<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), G, hidden,

@@ -58,7 +58,7 @@ class ed_plan_opts_t(ctypes.Structure):
 
 _INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bound", "num_rows", "hidden", "dtype",
              "workspace_bytes", "contig_operands", "gather_operands", "copy_bytes", "copy_kernels", "off_h",
-             "off_c", "off_y", "y_cols", "off_x", "off_ts")
+             "off_c", "off_y", "y_cols", "off_x", "off_ts", "off_u", "off_m")
 
 
 class ed_plan_info_t(ctypes.Structure):
@@ -255,7 +255,11 @@ class DeviceWeights:
                                               torch.from_numpy(p[wk]).to(device), stream)
                     if bk:
                         d["b2"] = torch.from_numpy(np.asarray(p[bk], np.float32)).to(device)
-                for k in ("emb", "emb2", "mat"):
+                if "mat" in p:  # MV-RNN word matrices: packed (transposed) by the library
+                    mat = np.asarray(p["mat"], np.float32)
+                    d["mat"] = ed_pack_weights(t.kind, t.hidden, mat.shape[0], t.dtype, 2,
+                                               torch.from_numpy(mat).to(device), stream)
+                for k in ("emb", "emb2"):
                     if k in p:
                         d[k] = torch.from_numpy(np.asarray(p[k], np.float32)).to(device=device, dtype=dt).contiguous()
             self.tensors.append(d)
@@ -306,6 +310,23 @@ class Workspace:
         if i["off_x"] < 0:
             return None
         return self._view(i["off_x"], i["num_rows"] * i["hidden"], torch.float32).view(i["num_rows"], i["hidden"])
+
+    def U(self) -> Optional[torch.Tensor]:
+        """MV-RNN matvec rows [num_rows, 2h] = [B a; A b] (None without MV-RNN types)."""
+        i = self.plan_info
+        if i["off_u"] < 0:
+            return None
+        dt = torch.bfloat16 if i["dtype"] == ED_BF16 else torch.float32
+        return self._view(i["off_u"], i["num_rows"] * 2 * i["hidden"], dt).view(i["num_rows"], 2 * i["hidden"])
+
+    def M(self) -> Optional[torch.Tensor]:
+        """MV-RNN node matrices [num_rows, h, h], each stored transposed (M[r] = P_r^T)."""
+        i = self.plan_info
+        if i["off_m"] < 0:
+            return None
+        dt = torch.bfloat16 if i["dtype"] == ED_BF16 else torch.float32
+        h = i["hidden"]
+        return self._view(i["off_m"], i["num_rows"] * h * h, dt).view(i["num_rows"], h, h)
 
     def step_times_ns(self) -> np.ndarray:
         """Per device step: time from the completion of all earlier steps to this step's completion

@@ -44,7 +44,9 @@ def compare(wl, plan, ws, out, instances=None):
     C = ws.C().cpu().numpy()
     Y = ws.Y().cpu().numpy() if plan.info["y_cols"] else None
     X = ws.X().cpu().numpy() if ws.X() is not None else None
-    ys, rs = {"h": [], "c": [], "y": [], "l": []}, {"h": [], "c": [], "y": [], "l": []}
+    Mx = ws.M()   # MV-RNN node matrices, stored transposed (compared when small enough to copy)
+    Mx = Mx.float().cpu().numpy() if Mx is not None and Mx.numel() <= (1 << 27) else None
+    ys, rs = {"h": [], "c": [], "y": [], "l": [], "M": []}, {"h": [], "c": [], "y": [], "l": [], "M": []}
     for k, gi in enumerate(idx):
         base = m.base[gi]
         for v, rec in recs[k].items():
@@ -53,6 +55,8 @@ def compare(wl, plan, ws, out, instances=None):
                 ys["h"].append(H[r]); rs["h"].append(rec["h"])
             if rec.get("c") is not None:
                 ys["c"].append(C[r]); rs["c"].append(rec["c"])
+            if rec.get("M") is not None and Mx is not None:
+                ys["M"].append(Mx[r].T.ravel()); rs["M"].append(np.asarray(rec["M"]).ravel())
             if rec.get("l") is not None:
                 ys["l"].append(X[r]); rs["l"].append(rec["l"])
             if rec.get("y") is not None:

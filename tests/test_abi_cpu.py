@@ -56,6 +56,7 @@ def _check_schedule(wl, priority=None):
     lambda: W.treelstm(32, (1, 30), 64, "bf16", cfg=9),
     lambda: W.treelstm(20, (1, 25), 64, "fp32", cfg=10, cell="treegru"),
     lambda: W.treefc(40, (1, 30), 64, "bf16", cfg=4),
+    lambda: W.treefc(40, (1, 30), 64, "bf16", cfg=4, cell="mvrnn"),
     lambda: W.bilstm(16, (1, 20), 64, "bf16", with_tagger=False),
 ])
 def test_schedule_bit_exact_with_oracle(wlf):
@@ -206,3 +207,26 @@ def test_empty_and_degenerate_graphs():
     one = W.graph_from_lists([0], [[-1, -2]])
     plan = E.ed_plan([empty, one, empty], t, fsm)
     assert plan.info["num_nodes"] == 1 and plan.info["num_batches"] == 1 and plan.info["num_instances"] == 3
+
+
+def test_mvrnn_plan_lowering_and_buffers():
+    """MV-RNN batches lower to three device steps (matvecs, p GEMM, matrix GEMM); the workspace holds
+    U [rows, 2h] and the node matrices [rows, h, h]; the word-matrix table packs to words*h*h."""
+    wl = W.treefc(12, (2, 9), 64, "bf16", cfg=4, cell="mvrnn")
+    plan = _plan(wl)
+    i = plan.info
+    assert i["num_steps"] == 3 * i["num_batches"]
+    assert i["off_u"] > 0 and i["off_m"] > i["off_u"]
+    rows, h = i["num_rows"], i["hidden"]
+    assert i["workspace_bytes"] >= i["off_m"] + 2 * rows * h * h
+    assert E.ed_packed_bytes("mvrnn_internal", 64, 100, "bf16", 2) == 100 * 64 * 64 * 2
+    assert E.ed_packed_bytes("mvrnn_internal", 64, 0, "fp32", 1) == 64 * 128 * 4
+    plain = _plan(W.treefc(12, (2, 9), 64, "bf16", cfg=4)).info
+    assert plain["off_u"] == -1 and plain["off_m"] == -1
+
+
+def test_mvrnn_rejects_bad_hidden():
+    t = [W.OpType("I", "mvrnn_internal", 2, weight_set=0, hidden=4100, dtype="fp32")]
+    g = W.treefc(2, (2, 4), 8, "fp32", cfg=4).graphs
+    with pytest.raises(E.EdError):
+        E.ed_plan(g, t, E.fsm_from_priority([0], 1))

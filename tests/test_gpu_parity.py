@@ -60,6 +60,22 @@ def test_treefc_with_external_leaves_and_single_leaf_instances(dtype, h):
     _check(wl)
 
 
+@pytest.mark.parametrize("dtype,h", [("bf16", 64), ("bf16", 128), ("bf16", 192), ("fp32", 32)])
+def test_mvrnn(dtype, h):
+    """MV-RNN: p (h), node matrices P (compared transposed back), roots.  h = 64: a 128-row tile of
+    the matrix product spans two nodes; h = 192: tiles straddle node blocks at 64-row granularity."""
+    wl = W.treefc(10, (1, 12), h, dtype, cfg=45, cell="mvrnn")
+    plan, w, ws, out, err = _check(wl)
+    assert "M" in err and "h" in err
+
+
+def test_cfg4_mvrnn_full_size_sampled():
+    """BASELINE cfg4 MV-RNN (1024 trees, h = 512, bf16) in bench.py's launch configuration; the oracle
+    evaluates sampled instances (4h^3 = 537 MFLOP per node in fp64)."""
+    wl = W.config("cfg4_mvrnn")
+    _check(wl, list(range(0, 1024, 97)))
+
+
 @pytest.mark.parametrize("dtype,h", [("bf16", 128), ("fp32", 64)])
 def test_bilstm_chains(dtype, h):
     _check(W.bilstm(20, (1, 30), h, dtype, cfg=42, with_tagger=False))
