@@ -1031,6 +1031,21 @@ __device__ __forceinline__ int step_items(const DevStep &st, int h) {
   if (is_umma_cell(st.cell)) return ((st.m + kTileM - 1) / kTileM) * st.n_col_tiles;
   return (st.m + kSimtRows - 1) / kSimtRows;
 }
+// K chunks per pipeline stage.  One full/empty mbarrier round costs ~0.3 us whatever its payload
+// (scripts/loop_probe.cu), so a small tile (m <= 120 rows: A chunk = round8(m) x 128 B) packs
+// several K chunks into one 48 KB stage: chunk q's A at q * abytes, its B at 16 KB + q * N * 128 B.
+// M = 128 MMAs read 128 A rows from q * abytes; rows past the tile's m are never stored.
+#ifndef ED_KPS_MAX
+#define ED_KPS_MAX 16
+#endif
+__device__ __forceinline__ int step_kps(const DevStep &st, int kc_total, uint32_t *abytes) {
+  if (st.cell == kCellMvMat) { *abytes = kAStage; return 1; }
+  const int rows = min(kTileM, (st.m + 7) & ~7);
+  *abytes = static_cast<uint32_t>(rows) * 128u;
+  const int bb = st.gates * st.units * 128;
+  const int k = min(kAStage / static_cast<int>(*abytes), kBStage / bb);
+  return max(1, min(min(k, kc_total), ED_KPS_MAX));
+}
 __device__ __forceinline__ int first_item(uint32_t off) {
   return static_cast<int>((blockIdx.x + gridDim.x - off % gridDim.x) % gridDim.x);
 }
@@ -1107,6 +1122,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     }
     const int ncols = st.gates * st.units;
     const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
+    uint32_t abytes = kAStage;
+    const int kps = step_kps(st, kc_total, &abytes);
+    const uint32_t bchunk = static_cast<uint32_t>(ncols) * 128u;
     if (warp < 4) {
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
@@ -1162,17 +1180,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
           tc_fence_after();
           const uint32_t d = tmem_base + acc * 256u;
-          for (int kc = 0; kc < kc_total; ++kc) {
+          for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
+            const int nk = min(kps, kc_total - kc0);
             const uint32_t stg = pipe.it % kStages;
             mbar_wait(full + stg, (pipe.it / kStages) & 1u);
             tc_fence_after();
-            ED_TRACE(p, s, 3, kc == 0 && t == t0);
-            const uint32_t a_addr = smem_u32(stages + stg * kStageBytes);
-            const uint32_t b_addr = a_addr + kAStage;
-            const uint64_t ad = sw128_desc(a_addr), bd = sw128_desc(b_addr);
+            ED_TRACE(p, s, 3, kc0 == 0 && t == t0);
+            const uint32_t sbase = smem_u32(stages + stg * kStageBytes);
+            for (int q = 0; q < nk; ++q) {
+              const uint64_t ad = sw128_desc(sbase + q * abytes), bd = sw128_desc(sbase + kAStage + q * bchunk);
 #pragma unroll
-            for (int k = 0; k < kChunkK / 16; ++k)
-              tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < kChunkK / 16; ++k)
+                tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc0 + q > 0 || k > 0) ? 1u : 0u);
+            }
             tc_commit(empty + stg);
             ++pipe.it;
           }
@@ -1189,13 +1209,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       for (int t = t0; t < T; t += G) {
         const int col_tile = t % st.n_col_tiles;
         if (lane == 0) {
-          for (int kc = 0; kc < kc_total; ++kc) {
+          const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
+          for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
+            const int nk = min(kps, kc_total - kc0);
             const uint32_t stg = pipe.it % kStages;
             mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
-            const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
-            mbar_arrive_tx(full + stg, nb);
-            const uint8_t *src = Wp + ((static_cast<size_t>(kc) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-            bulk_g2s(stages + stg * kStageBytes + kAStage, src, nb, full + stg);
+            mbar_arrive_tx(full + stg, nb * nk);
+            for (int q = 0; q < nk; ++q) {
+              const uint8_t *src =
+                  Wp + ((static_cast<size_t>(kc0 + q) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
+              bulk_g2s(stages + stg * kStageBytes + kAStage + q * bchunk, src, nb, full + stg);
+            }
             ++pipe.it;
           }
         }
@@ -1289,9 +1313,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA below
         if (lt == 0) ED_TRACE(p, s, 1, t == t0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
-        for (int kc = 0; kc < kc_total; ++kc) {
+        for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
+          const int nk = min(kps, kc_total - kc0);
           const uint32_t stg = pipe.it % kStages;
           mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+          if (nk > 1) {  // several small chunks per stage: row gathers only (a 128-row box would overflow)
+            if (lt == 0) mbar_arrive(full + stg);
+            for (int q = 0; q < nk; ++q) {
+              const int kc = kc0 + q;
+              const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
+              const uint32_t a_base = smem_u32(stages + stg * kStageBytes) + q * abytes;
+              for (int c = lt; c < nrows * 8; c += kLoaderThreads) {
+                const int r = c >> 3, ch = c & 7;
+                const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
+                cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
+              }
+            }
+          } else {
+          const int kc = kc0;
           const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
           uint8_t *a_dst = stages + stg * kStageBytes;
           int cbase = -1;
@@ -1311,6 +1350,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
               const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
               cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
             }
+          }
           }
           cp_async_commit();
           if (++cp_pending == kLag) {

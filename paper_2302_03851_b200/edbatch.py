@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libedbatch.so")
+LIB_PATH = os.environ.get("ED_BATCH_LIB") or os.path.join(_HERE, "libedbatch.so")  # override: A/B builds
 
 ED_OK = 0
 ED_ZERO_INPUT = -(2 ** 31)
