@@ -44,7 +44,7 @@ constexpr int kBiasBytes = 5 * 512 * 4;           // G * h fp32 (G * h <= 2560)
 constexpr int kWoutBytes = 12 * 1024;             // output-linear weights [C][h] fp32 (else read from L2)
 constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes + kWoutBytes + 256;
 constexpr int kEpiThreads = 128;
-constexpr int kLag = 3;  // cp.async groups in flight before a stage is released (< kStages)
+
 
 // ------------------------------------------------------------------------------------------------
 // PTX helpers
@@ -102,6 +102,11 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// The mbarrier receives one arrival once every cp.async this thread issued so far has landed (the
+// barrier's expected count includes it: .noinc).
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -244,8 +249,9 @@ __device__ __forceinline__ void stamp_step(const KParams &p, int s) {
 }
 
 // optional phase trace of CTA 0 (profiling aid)
+// phase stamps of the CTA that runs item 0 of each step (profiling aid; off unless io.trace is set)
 #define ED_TRACE(p, s, k, first) \
-  do { if ((p).trace && blockIdx.x == 0 && (first)) (p).trace[(s) * 64 + (k)] = globaltimer(); } while (0)
+  do { if ((p).trace && (first)) (p).trace[(s) * 64 + (k)] = globaltimer(); } while (0)
 
 // ------------------------------------------------------------------------------------------------
 // cell math — one hidden unit, fp32
@@ -816,7 +822,7 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4 &v, float *out) {
 template <int CELL>
 __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
                                               uint32_t parity, int row_tile, int col_tile, int r,
-                                              const float *sbias) {
+                                              const float *sbias, unsigned long long *tr = nullptr) {
   using CC = CellCfg<CELL>;
   constexpr int G = CC::G, NC = CC::NC, NH = CC::NH;
   const int h = p.hidden;
@@ -855,6 +861,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   for (int q = 0; q < NH; ++q) hn[q] = __ldcg(q == 0 ? hp0 : hp1);
   mbar_wait(tfull_bar, parity);
   tc_fence_after();
+  if (tr != nullptr && r == 0) *tr = globaltimer();
   __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
   const size_t orow = static_cast<size_t>(st.out_row0 + (valid ? i : 0));
   const int nsteps = ngroups * 2;
@@ -1065,7 +1072,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 2 + kLoaderThreads / 32);  // A TMA-or-nothing + loader warps + B (expect_tx)
+      mbar_init(full + s, 2 + kLoaderThreads);  // A TMA-or-nothing + every loader thread's cp.async + B
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -1088,7 +1095,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   const int G = static_cast<int>(gridDim.x);
   Pipe pipe;
   uint32_t tab_tile = 0;    // loader threads: row-table buffer toggle
-  uint32_t cp_pending = 0;  // loader warps: committed cp.async groups not yet released
   uint32_t off = 0;         // running item offset (work rotation)
 
   // Every warp role walks the steps in order; there is no grid barrier between steps (dataflow).
@@ -1098,7 +1104,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const int t0 = first_item(off);
     off = (off + static_cast<uint32_t>(T)) % static_cast<uint32_t>(G);
     if (t0 >= T) continue;  // no work for this CTA in this step
-    ED_TRACE(p, s, 0, tid == 0);
+    ED_TRACE(p, s, 0, tid == 0 && t0 == 0);
     if (!is_umma_cell(st.cell)) {
       if (st.cell == ED_CELL_MVRNN_INTERNAL) {  // ---- MV-RNN matvecs: one CTA per item ----
         __syncthreads();  // sbias / swout are free (previous step's epilogue done)
@@ -1140,31 +1146,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         const uint32_t par = (pipe.ti >> 1) & 1u;
         switch (st.cell) {
           case ED_CELL_TREELSTM_LEAF:
-            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREELSTM_INTERNAL:
-            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEGRU_LEAF:
-            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEGRU_INTERNAL:
-            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEFC_INTERNAL:
-            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LSTM:
-            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_CHAR:
-            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_WORD:
-            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellLatticeLink:
-            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvP:
-            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvMat:
             mv_mat_epilogue(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid); break;
           default:
-            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias); break;
+            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
         }
-        ED_TRACE(p, s, 5, tid == 0 && t == t0);
+        ED_TRACE(p, s, 5, tid == 0 && t == 0);
         tc_fence_before();
         mbar_arrive(tempty + acc);
         ++pipe.ti;
@@ -1184,8 +1190,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             const int nk = min(kps, kc_total - kc0);
             const uint32_t stg = pipe.it % kStages;
             mbar_wait(full + stg, (pipe.it / kStages) & 1u);
+            fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
             tc_fence_after();
-            ED_TRACE(p, s, 3, kc0 == 0 && t == t0);
+            ED_TRACE(p, s, 3, kc0 == 0 && t == 0);
             const uint32_t sbase = smem_u32(stages + stg * kStageBytes);
             for (int q = 0; q < nk; ++q) {
               const uint64_t ad = sw128_desc(sbase + q * abytes), bd = sw128_desc(sbase + kAStage + q * bchunk);
@@ -1197,7 +1204,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             ++pipe.it;
           }
           tc_commit(tfull + acc);
-          ED_TRACE(p, s, 4, t == t0);
+          ED_TRACE(p, s, 4, t == 0);
         }
         ++pipe.ti;
       }
@@ -1229,8 +1236,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- operand (A) loaders: warps 6-11 ----------------
       // Per tile: row table (static) -> wait until every input row is published (acquire) ->
       // CONTIG operand: one TMA 128-row box; gathered operand: 16 B cp.async per (row, chunk).
-      // Stages are released to the MMA with a lag of kLag groups and drained at the end of every
-      // tile (a later tile may wait for rows this CTA's epilogue still has to produce).
+      // Every loader thread hands its part of a stage to the MMA with cp.async.mbarrier.arrive.noinc
+      // (the stage completes when all gathered rows and TMA bytes have landed); the MMA thread fences
+      // the generic -> async proxy before reading the stage.
       const int lt = tid - 192;  // 0 .. kLoaderThreads-1
       const int nseg = cell_segments_dev(st.cell);
       if (st.cell == kCellMvMat) {
@@ -1273,8 +1281,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
                   tma_row_box(a_dst + q * 8192, &p.tm_mat[st.wset], col0, (-1 - e) * h + rr0[q], full + stg);
               }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full + stg);
+            cp_async_arrive_noinc(full + stg);
             ++pipe.it;
           }
         }
@@ -1311,7 +1318,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA below
-        if (lt == 0) ED_TRACE(p, s, 1, t == t0);
+        if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
         for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
           const int nk = min(kps, kc_total - kc0);
@@ -1352,24 +1359,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             }
           }
           }
-          cp_async_commit();
-          if (++cp_pending == kLag) {
-            cp_async_wait<kLag - 1>();
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full + (pipe.it + 1 - kLag) % kStages);
-            --cp_pending;
-          }
+          // the stage completes when this thread's gathers have landed (no software lag)
+          cp_async_arrive_noinc(full + stg);
           ++pipe.it;
         }
-        // drain: the tile's last stages must reach the MMA now (its rows may be awaited by other
-        // CTAs, and this CTA's next tile may be many steps away)
-        cp_async_wait<0>();
-        fence_proxy_async_smem();
-        __syncwarp();
-        for (; cp_pending > 0; --cp_pending)
-          if (lane == 0) mbar_arrive(full + (pipe.it - cp_pending) % kStages);
-        if (lt == 0) ED_TRACE(p, s, 2, t == t0);
+        if (lt == 0) ED_TRACE(p, s, 2, t == 0);
       }
     }
   }

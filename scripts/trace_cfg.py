@@ -1,4 +1,5 @@
-"""Per-phase trace of CTA 0 for each batch of a config (development aid)."""
+"""Per-phase trace of the CTA that runs item 0 of each device step (development aid).
+Times in ns relative to the end of the previous step (max over CTAs of its last item)."""
 import sys
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import numpy as np, torch
@@ -11,18 +12,16 @@ plan, w, ws, out = run_gpu(wl)
 nb = plan.info["num_steps"]
 tr = torch.zeros(nb * 64, dtype=torch.int64, device="cuda")
 for _ in range(3):
+    tr.zero_()
     E.ed_execute(plan, w, ws, out, trace=tr)
 torch.cuda.synchronize()
 t = tr.view(nb, 64).cpu().numpy().astype(np.int64)
+i = ws.plan_info
+ts = ws._view(i["off_ts"], nb + 1, torch.int64).cpu().numpy().astype(np.int64)
+end = np.maximum.accumulate(ts)
 sched = plan.schedule()
-print("phase stamps relative to step start (ns): [A-tab, A-issued, MMA-first-full, MMA-done, EPI-start, EPI-done, step-end]")
+print("phases rel. to previous step end (ns): reached, rows-ready, A-issued, MMA-1st-full, MMA-issued, EPI-got-acc, EPI-done | step end")
 for s in range(nb):
-    rel = [(int(t[s, k] - t[s, 0]) if t[s, k] else -1) for k in range(1, 8)]
-    print(s, wl.types[sched[s][0]].name, len(sched[s][1]), rel)
-for s in (1, 8, 13):
-    base = t[s, 0]
-    rel = lambda a, b: [int(t[s, k] - base) if t[s, k] else -1 for k in range(a, b)]
-    print(f"step {s}: MMA full-wait done per kc:", rel(8, 24))
-    print(f"step {s}: B issue per kc          :", rel(24, 40))
-    print(f"step {s}: A release per kc        :", rel(40, 56))
-print("step times:", ws.step_times_ns().tolist())
+    base = end[s]
+    rel = lambda k: int(t[s, k] - base) if t[s, k] else None
+    print(s, len(sched[min(s, len(sched) - 1)][1]), [rel(k) for k in (0, 1, 2, 3, 4, 6, 5)], "|", int(ts[s + 1] - base))
