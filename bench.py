@@ -246,6 +246,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layout", default="schedule", choices=["schedule", "pq"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--staging", default="auto", choices=["auto", "off"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -271,7 +272,8 @@ def main():
     wl = make_workload(args.config, rank, world, args.scaling)
     layout = E.ED_LAYOUT_PQ if args.layout == "pq" else E.ED_LAYOUT_SCHEDULE_ORDER
     fsm = E.fsm_from_priority(wl.priority, len(wl.types))
-    plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout)
+    staging = E.ED_STAGING_OFF if args.staging == "off" else E.ED_STAGING_AUTO
+    plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging)
     weights = E.DeviceWeights(wl.types, wl.params)
     ws = E.Workspace(plan)
     tdt = torch.bfloat16 if wl.dtype == "bf16" else torch.float32
@@ -321,7 +323,7 @@ def main():
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        p2 = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout)   # host scheduling + layout
+        p2 = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging)   # host scheduling + layout
         ws.plan_info = p2.info
         E.ed_execute(p2, weights, ws, out)                         # uploads the step table (H2D)
         host_out.copy_(out, non_blocking=True)                     # D2H of the step's result

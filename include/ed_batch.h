@@ -70,7 +70,9 @@ typedef int32_t ed_status_t;
 #define ED_FALLBACK_KEY0 0  /* table miss or action not ready: take key[0] (reading A-3) */
 
 #define ED_LAYOUT_SCHEDULE_ORDER 0  /* rows in schedule order: results contiguous, sources gathered */
-#define ED_LAYOUT_PQ             1  /* PQ-tree plan (§3.2, Alg. 2-6) over the node-output rows      */
+#define ED_LAYOUT_PQ             1
+#define ED_STAGING_AUTO          0
+#define ED_STAGING_OFF           1  /* PQ-tree plan (§3.2, Alg. 2-6) over the node-output rows      */
 
 /* One op type ("each operation is given a type"). */
 typedef struct {
@@ -118,7 +120,12 @@ typedef struct {
 
 typedef struct {
   int32_t layout;        /* ED_LAYOUT_SCHEDULE_ORDER | ED_LAYOUT_PQ */
-  int32_t reserved[7];   /* must be 0 */
+  int32_t staging;       /* ED_STAGING_AUTO (0): bf16 plans stage gathered cell operands of large
+                            batches (the producer's epilogue also stores its h row into a
+                            contiguous operand block of the consuming batch, read by TMA);
+                            ED_STAGING_OFF (1): every non-contiguous operand is gathered row by
+                            row.  Results are bitwise identical. */
+  int32_t reserved[6];   /* must be 0 */
 } ed_plan_opts_t;
 
 typedef struct ed_plan_s ed_plan_t;  /* opaque plan handle */
@@ -149,6 +156,10 @@ typedef struct {
   double plan_us;             /* host time spent in ed_plan                               */
   double schedule_us;
   double layout_us;
+  int64_t staged_operands;    /* bf16: gathered (batch, slot) operands staged into contiguous   */
+                              /*   blocks by their producers' epilogues (read as TMA boxes)     */
+  int64_t staged_bytes;       /* bytes of those extra producer stores per execute               */
+  int64_t h_rows;             /* rows of the H buffer: num_rows + staged operand rows           */
 } ed_plan_info_t;
 
 /* Per weight set, device pointers.  Matrices must have been packed by ed_pack_weights.

@@ -147,6 +147,10 @@ struct ed_plan_s {
   bool need_mv = false;  // MV-RNN: U and Mx buffers
   // stats
   int64_t contig = 0, gather = 0, copy_bytes = 0, copy_kernels = 0;
+  bool staging = true;      // bf16: stage gathered cell operands into contiguous blocks
+  int64_t op_rows = 0;      // staged operand rows appended to H (rows V+1 ..)
+  int64_t staged = 0, staged_bytes = 0;
+  int64_t dst_base = 0;     // idx offset of dst_off[V + 2] (then the copy destinations)
   double plan_us = 0, sched_us = 0, layout_us = 0;
   // upload state
   std::vector<uint8_t> blob;          // [ts zeros | steps | idx | roots]
@@ -356,6 +360,9 @@ static ed_status_t lower(ed_plan_t *pl) {
     return x;  // external id
   };
   pl->steps.clear();
+  pl->op_rows = pl->staged = pl->staged_bytes = 0;
+  std::vector<std::pair<int32_t, int32_t>> stage_pairs;  // (producer row, staged H row)
+  const bool staging = pl->staging && pl->dtype == ED_BF16;
   for (int b = 0; b < nb; ++b) {
     const int t = pl->batch_type[b];
     const ed_op_type_t &ot = pl->types[t];
@@ -407,8 +414,30 @@ static ed_status_t lower(ed_plan_t *pl) {
         ++pl->gather;
         pl->copy_bytes += 2 * static_cast<int64_t>(m) * row_bytes;
         ++pl->copy_kernels;
+        // Staging (bf16 tensor-core cells whose slot j is an A operand, batches of >= 128 members
+        // where the loaders use 128-row TMA boxes): if every entry is a produced row (or the zero
+        // state), the batch gets a block of m H rows after the node records; each producer's
+        // epilogue also stores its h row there, and the loaders read the block as TMA boxes
+        // instead of gathering 16 B pieces of m scattered rows (~25 GB/s per SM on B200).
+        const bool a_operand = ed::cell_gates(ot.cell_kind) > 0 && ot.cell_kind != ED_CELL_MVRNN_INTERNAL &&
+                               !(ot.cell_kind == ED_CELL_LATTICE_WORD && j == 1);
+        bool ok = staging && a_operand && m >= 128;
+        for (int i = 0; i < m && ok; ++i) {
+          const int32_t raw = pl->in_idx[pl->in_off[mem[i]] + j];
+          ok = raw >= 0 || raw == ED_ZERO_INPUT;
+        }
+        if (ok) {
+          const int32_t base = static_cast<int32_t>(V + 1 + pl->op_rows);
+          pl->idx.push_back(base);
+          for (int i = 0; i < m; ++i)
+            if (ent[i] != zero_row) stage_pairs.emplace_back(ent[i], base + i);
+          pl->op_rows += m;
+          ++pl->staged;
+          pl->staged_bytes += static_cast<int64_t>(m) * row_bytes;
+          st.mode[j] = 2;
+        }
       }
-      pl->slot_modes[static_cast<size_t>(b) * 2 + j] = st.mode[j];
+      pl->slot_modes[static_cast<size_t>(b) * 2 + j] = st.mode[j] == 1 ? 1 : 0;
     }
     if (ot.has_ext) {
       st.ext_off = static_cast<int32_t>(pl->idx.size());
@@ -488,6 +517,18 @@ static ed_status_t lower(ed_plan_t *pl) {
       pl->steps.push_back(s2);
     }
   }
+  // copies of every result row into staged operand blocks (CSR over rows 0..V), appended to idx
+  {
+    std::vector<int32_t> cnt(V + 2, 0);
+    for (const auto &pr : stage_pairs) ++cnt[pr.first + 1];
+    for (int64_t r = 0; r <= V; ++r) cnt[r + 1] += cnt[r];
+    pl->dst_base = static_cast<int64_t>(pl->idx.size());
+    const int32_t base2 = static_cast<int32_t>(pl->dst_base + V + 2);
+    for (int64_t r = 0; r <= V + 1; ++r) pl->idx.push_back(base2 + cnt[r]);
+    pl->idx.resize(pl->idx.size() + stage_pairs.size());
+    std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+    for (const auto &pr : stage_pairs) pl->idx[base2 + fill[pr.first]++] = pr.second;
+  }
   // readiness: target[row] = sum of what every device step writing the row publishes; a step that
   // reads its own rows waits for what the earlier steps of its batch publish (self_need)
   pl->target.assign(V + 1, 0);
@@ -515,7 +556,7 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->off_roots = off; off = align_up(off + 4 * static_cast<size_t>(pl->ninst), 256);
   pl->off_target = off; off = align_up(off + 4 * static_cast<size_t>(rows), 256);
   pl->off_ready = off; off = align_up(off + 4 * static_cast<size_t>(rows), 1024);
-  pl->off_h = off; off = align_up(off + elt * rows * h, 1024);
+  pl->off_h = off; off = align_up(off + elt * (rows + pl->op_rows) * h, 1024);
   pl->off_c = off; off = align_up(off + 4 * rows * h, 1024);
   pl->y_cols = 0;
   pl->need_x = false;
@@ -560,11 +601,14 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   const int layout = opts ? opts->layout : ED_LAYOUT_SCHEDULE_ORDER;
   if (layout != ED_LAYOUT_SCHEDULE_ORDER && layout != ED_LAYOUT_PQ) return fail(ED_E_INVALID_ARG, "unknown layout");
   if (opts)
-    for (int k = 0; k < 7; ++k)
+    for (int k = 0; k < 6; ++k)
       if (opts->reserved[k] != 0) return fail(ED_E_INVALID_ARG, "opts.reserved must be 0");
+  if (opts && opts->staging != ED_STAGING_AUTO && opts->staging != ED_STAGING_OFF)
+    return fail(ED_E_INVALID_ARG, "unknown staging mode");
   ed_plan_t *pl = new (std::nothrow) ed_plan_t();
   if (!pl) return fail(ED_E_OOM, "out of host memory");
   pl->types.assign(types, types + num_types);
+  pl->staging = !(opts && opts->staging == ED_STAGING_OFF);
   pl->hidden = types[0].hidden;
   pl->dtype = types[0].dtype;
   for (int t = 0; t < num_types; ++t) {
@@ -661,6 +705,9 @@ ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
   o->plan_us = pl->plan_us;
   o->schedule_us = pl->sched_us;
   o->layout_us = pl->layout_us;
+  o->staged_operands = pl->staged;
+  o->staged_bytes = pl->staged_bytes;
+  o->h_rows = pl->V + 1 + pl->op_rows;
   return ED_OK;
 }
 
@@ -740,7 +787,8 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
     if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_bar, 0, pl->off_ts - pl->off_bar, s);  // barrier flags
     if (ce == cudaSuccess) {
       const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
-      ce = cudaMemsetAsync(base + pl->off_h + elt * pl->V * pl->hidden, 0, elt * pl->hidden, s);
+      // zero row V and the staged rows (zero-state entries are never written by a producer)
+      ce = cudaMemsetAsync(base + pl->off_h + elt * pl->V * pl->hidden, 0, elt * pl->hidden * (1 + pl->op_rows), s);
       if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_c + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
       if (ce == cudaSuccess && pl->need_x)
         ce = cudaMemsetAsync(base + pl->off_x + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
@@ -774,6 +822,7 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   p.ts = reinterpret_cast<unsigned long long *>(base + pl->off_ts);
   p.ready = reinterpret_cast<int *>(base + pl->off_ready);
   p.target = reinterpret_cast<const int *>(base + pl->off_target);
+  p.dst_off = p.idx + pl->dst_base;
   {  // per launch: readiness counters and step stamps start from zero
     cudaError_t ce = cudaMemsetAsync(p.ready, 0, 4 * static_cast<size_t>(pl->V + 1), s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(p.ts, 0, 8 * (pl->steps.size() + 1), s);
@@ -801,7 +850,7 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   }
   if (pl->dtype == ED_BF16) {
     const int64_t hh = pl->hidden;
-    if (!encode_rows(&p.tm_h128, p.H, pl->V + 1, hh, 128))
+    if (!encode_rows(&p.tm_h128, p.H, pl->V + 1 + pl->op_rows, hh, 128))
       return fail(ED_E_CUDA, "cuTensorMapEncodeTiled failed for the H buffer");
     if (pl->need_mv) {
       if (!encode_rows(&p.tm_u, p.U, pl->V + 1, 2 * hh, 128) || !encode_rows(&p.tm_mx, p.Mx, (pl->V + 1) * hh, hh, 64))

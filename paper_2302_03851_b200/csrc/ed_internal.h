@@ -26,6 +26,9 @@ constexpr int kMaxSlotsDev = 2;   // fixed slots the device reads (all cells hav
 // Slot j of member i (position i = ascending result row):
 //   mode[j] == 1 (CONTIG): entry = arg[j] + i             (one contiguous aligned block)
 //   mode[j] == 0 (GATHER): entry = idx[arg[j] + i]
+//   mode[j] == 2 (STAGED): entry = idx[arg[j] + i] as for GATHER, and the A operand of the slot is
+//                          read from H rows idx[arg[j] + m] + i: a block the producers' epilogues
+//                          fill with copies of their h rows (bf16 tensor-core cells only)
 // An entry >= 0 is a row of the H/C/X buffers (the zero row for ED_ZERO_INPUT); an entry < 0 is
 // an external id (-1 - id) read from the weight set's embedding table.
 struct DevStep {
@@ -78,6 +81,7 @@ struct alignas(64) KParams {
   unsigned long long *ts;     // [num_steps + 1]
   void *out_root;             // [num_inst x hidden] or null
   unsigned long long *trace;  // [num_steps x 64] phase stamps of CTA 0, or null
+  const int32_t *dst_off;     // [rows + 1] staged-operand copies of each result row (CSR into idx)
   int *ready;                 // [rows] hidden units published per row (zeroed every launch)
   const int *target;          // [rows] units a row holds when final (sum of step_contrib)
   int32_t num_steps;

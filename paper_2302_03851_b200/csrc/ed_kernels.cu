@@ -278,7 +278,7 @@ template <typename T> __device__ __forceinline__ float act_exp(float x) { return
 template <> __device__ __forceinline__ float act_exp<float>(float x) { return expf(x); }
 
 __device__ __forceinline__ int slot_entry(const DevStep &st, const int32_t *idx, int j, int i) {
-  return st.mode[j] ? st.arg[j] + i : __ldg(idx + st.arg[j] + i);
+  return st.mode[j] == 1 ? st.arg[j] + i : __ldg(idx + st.arg[j] + i);
 }
 
 template <typename T>
@@ -344,7 +344,7 @@ __device__ __forceinline__ int segment_entry(const KParams &p, const DevStep &st
   return slot_entry(st, p.idx, s, i);
 }
 // Whether K segment s is one contiguous block of H rows (layout plan made it adjacent + aligned).
-__device__ __forceinline__ bool segment_contig(const DevStep &st, int s, int *base) {
+__device__ __forceinline__ bool segment_contig(const KParams &p, const DevStep &st, int s, int *base) {
   if (st.cell == kCellMvP) {  // the node's own U rows: always one block
     *base = st.out_row0;
     return true;
@@ -354,8 +354,12 @@ __device__ __forceinline__ bool segment_contig(const DevStep &st, int s, int *ba
     if (s == 0) return false;
     slot = 0;
   }
+  if (st.mode[slot] == 2) {  // staged block (rows written by the producers' epilogues)
+    *base = __ldg(p.idx + st.arg[slot] + st.m);
+    return true;
+  }
   *base = st.arg[slot];
-  return st.mode[slot] != 0;
+  return st.mode[slot] == 1;
 }
 
 __device__ __forceinline__ float c_of(const KParams &p, int e, int j) {
@@ -842,6 +846,12 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   const float4 *cp0 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e0) * h + jb);
   const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1) * h + jb);
   const __nv_bfloat16 *Hb = static_cast<const __nv_bfloat16 *>(p.H);
+  int dbeg = 0, dend = 0, d0 = -1;  // staged-operand copies of this result row (first one in a register)
+  if (valid && CELL != kCellLatticeLink) {
+    dbeg = __ldg(p.dst_off + st.out_row0 + i);
+    dend = __ldg(p.dst_off + st.out_row0 + i + 1);
+    if (dbeg < dend) d0 = __ldg(p.idx + dbeg++);
+  }
   const uint4 *hp0 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e0) * h + jb);
   const uint4 *hp1 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e1) * h + jb);
   // lattice char: words ending here (variadic inputs)
@@ -974,7 +984,11 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
         __nv_bfloat162 t = __floats2bfloat162_rn(hv[2 * k], hv[2 * k + 1]);
         packed[k] = *reinterpret_cast<uint32_t *>(&t);
       }
-      *reinterpret_cast<uint4 *>(H + orow * h + j0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      const uint4 hv4 = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      *reinterpret_cast<uint4 *>(H + orow * h + j0) = hv4;
+      if (d0 >= 0) *reinterpret_cast<uint4 *>(H + static_cast<size_t>(d0) * h + j0) = hv4;
+      for (int d = dbeg; d < dend; ++d)
+        *reinterpret_cast<uint4 *>(H + static_cast<size_t>(__ldg(p.idx + d)) * h + j0) = hv4;
     }
     if constexpr (HAS_C) {
       float *dst = (CELL == kCellLatticeLink) ? p.X : p.C;
@@ -1341,7 +1355,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
           uint8_t *a_dst = stages + stg * kStageBytes;
           int cbase = -1;
-          if (segment_contig(st, seg, &cbase)) {
+          if (segment_contig(p, st, seg, &cbase)) {
             if (lt == 0) {
               mbar_arrive_tx(full + stg, kAStage);
               if (st.cell == kCellMvP)  // U rows: [B a | A b], 2h columns

@@ -21,6 +21,7 @@ ED_ZERO_INPUT = -(2 ** 31)
 ED_FP32, ED_BF16 = 0, 1
 ED_ENC_SORT, ED_ENC_BASE = 0, 1
 ED_LAYOUT_SCHEDULE_ORDER, ED_LAYOUT_PQ = 0, 1
+ED_STAGING_AUTO, ED_STAGING_OFF = 0, 1
 STATUS = {0: "ED_OK", -1: "ED_E_INVALID_ARG", -2: "ED_E_CYCLE", -3: "ED_E_DANGLING", -4: "ED_E_DUP_ID",
           -5: "ED_E_TYPE", -6: "ED_E_ARITY", -7: "ED_E_FSM", -8: "ED_E_CUDA", -9: "ED_E_UNSUPPORTED",
           -10: "ED_E_WORKSPACE", -11: "ED_E_OOM"}
@@ -53,7 +54,7 @@ class ed_fsm_t(ctypes.Structure):
 
 
 class ed_plan_opts_t(ctypes.Structure):
-    _fields_ = [("layout", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+    _fields_ = [("layout", ctypes.c_int32), ("staging", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 _INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bound", "num_rows", "hidden", "dtype",
@@ -63,7 +64,8 @@ _INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bo
 
 class ed_plan_info_t(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in _INFO_I64] + [
-        ("plan_us", ctypes.c_double), ("schedule_us", ctypes.c_double), ("layout_us", ctypes.c_double)]
+        ("plan_us", ctypes.c_double), ("schedule_us", ctypes.c_double), ("layout_us", ctypes.c_double),
+        ("staged_operands", ctypes.c_int64), ("staged_bytes", ctypes.c_int64), ("h_rows", ctypes.c_int64)]
 
 
 class ed_weight_set_t(ctypes.Structure):
@@ -184,7 +186,7 @@ class Plan:
 
 
 def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: int = ED_ENC_SORT,
-            layout: int = ED_LAYOUT_SCHEDULE_ORDER) -> Plan:
+            layout: int = ED_LAYOUT_SCHEDULE_ORDER, staging: int = 0) -> Plan:
     """graphs: objects with numpy fields type/in_off/in_idx/ext and int root (workloads.Graph);
     types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype."""
     keep = []
@@ -203,7 +205,7 @@ def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: in
         keep.append(ka)
         earr[k] = ed_fsm_entry_t(len(ka), _ptr(ka), int(act))
     f = ed_fsm_t(encoder, len(fsm), earr, 0)
-    opts = ed_plan_opts_t(layout, (ctypes.c_int32 * 7)())
+    opts = ed_plan_opts_t(layout, staging, (ctypes.c_int32 * 6)())
     h = ctypes.c_void_p()
     _check(LIB.ed_plan(garr, len(graphs), tarr, len(types), ctypes.byref(f), ctypes.byref(opts), ctypes.byref(h)))
     return Plan(h, len(types))
