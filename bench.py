@@ -35,10 +35,10 @@ METRICS = {"cfg3": METRIC,
            "cfg4_treefc": "instances/sec TreeFC h=512 (cfg4: 1024 trees, bf16) per step, whole job",
            "cfg4_mvrnn": "instances/sec MV-RNN h=512 (cfg4: 1024 trees, bf16) per step, whole job"}
 CONFIGS = {
-    "cfg3": "cfg3 TreeLSTM h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16, FSM L>I>O",
+    "cfg3": "cfg3 TreeLSTM h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
     "cfg3_gru": "cfg3 TreeGRU h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
     "cfg1": "cfg1 TreeLSTM h=32, 8 random trees (leaves U[2,16]), fp32",
-    "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16, FSM F>B>T",
+    "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16",
     "cfg5": "cfg5 LatticeLSTM h=256, 512 character lattices (chars U[10,50], word p=0.3), bf16",
     "cfg4_treefc": "cfg4 TreeFC h=512, 1024 random trees (leaves U[5,40]), bf16",
     "cfg4_mvrnn": "cfg4 MV-RNN h=512, 1024 random trees (leaves U[5,40], 1024 word vectors + matrices), bf16",
@@ -247,6 +247,7 @@ def main():
     ap.add_argument("--layout", default="schedule", choices=["schedule", "pq"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--staging", default="auto", choices=["auto", "off"])
+    ap.add_argument("--fsm", default="learned", choices=["learned", "priority"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -271,7 +272,13 @@ def main():
 
     wl = make_workload(args.config, rank, world, args.scaling)
     layout = E.ED_LAYOUT_PQ if args.layout == "pq" else E.ED_LAYOUT_SCHEDULE_ORDER
-    fsm = E.fsm_from_priority(wl.priority, len(wl.types))
+    fsm_info = {"fsm": args.fsm}
+    if args.fsm == "learned":  # PAPER §2.3: Q-learned per topology, offline, not timed
+        learned = E.ed_fsm_learn(wl.graphs, wl.types)
+        fsm = learned.table
+        fsm_info.update(fsm_episodes=learned.info["episodes"], fsm_learn_ms=round(learned.info["learn_us"] / 1e3, 3))
+    else:
+        fsm = E.fsm_from_priority(wl.priority, len(wl.types))
     staging = E.ED_STAGING_OFF if args.staging == "off" else E.ED_STAGING_AUTO
     plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging)
     weights = E.DeviceWeights(wl.types, wl.params)
@@ -359,7 +366,7 @@ def main():
             "metric": METRICS[args.config], "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded parse-like trees, random-init weights)",
-            "config": {"workload": CONFIGS[args.config], "instances_per_gpu": len(wl.graphs),
+            "config": {"workload": CONFIGS[args.config], **fsm_info, "instances_per_gpu": len(wl.graphs),
                        "nodes_per_gpu": wl.num_nodes, "batches": plan.info["num_batches"],
                        "lower_bound": plan.info["lower_bound"], "layout": args.layout,
                        "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world} ({args.scaling}; LPT by node count when strong)"},

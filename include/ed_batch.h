@@ -239,6 +239,63 @@ int64_t ed_plan_upload_bytes(const ed_plan_t *plan);
 /* Number of kernels ed_execute launches (for launch accounting). */
 int32_t ed_execute_launch_count(const ed_plan_t *plan);
 
+/* ---------------------------------------------------------------------------------------------
+ * Learning the FSM (PAPER §2.3 "Using RL to Learn the FSM"; §5.3): tabular
+ * N-step Q-learning over the instance graphs, one instance per episode (episodes cycle over the
+ * graphs).  State = E(G_t) (ED_ENC_SORT or ED_ENC_BASE), action = the next batch's type (all
+ * ready nodes of it, Alg. 1), reward Eq. 1 r = -1 + alpha * |Frontier_a(G_t)| / |Frontier(G^a_t)|
+ * (the ratio read as in DESIGN.md A-1).  After each episode, for t = 0..T-1 in order:
+ *   Q(S_t,a_t) += lr * (sum_{i<N, t+i<T} r_{t+i} + [t+N<T] max_b Q(S_{t+N},b) - Q(S_t,a_t))
+ * (b over the types present in S_{t+N}; unseen pairs count 0; no discount).  Actions are
+ * epsilon-greedy over the ready types: one SplitMix64 draw x, u = (x >> 11) * 2^-53; u < eps takes
+ * ready[y % #ready] for a second draw y (ready types ascending), else argmax Q (ties: lowest id);
+ * eps = max(eps_floor, eps0 * eps_decay^(episode / eps_every)).  Every check_every episodes the
+ * greedy table is evaluated with Alg. 1 (A-3 fallback for unseen states) on all instances and
+ * training stops when the batch total reaches the App. B.3 lower bound (sum over instances).
+ * The result is an FSM table for ed_plan (state -> argmax_a Q) plus the Q values.
+ * Host only; deterministic for a given seed; no CUDA call. ------------------------------------ */
+typedef struct {
+  int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE                                            */
+  int32_t n_steps;       /* N >= 1 (bootstrapping horizon)                                        */
+  int32_t max_episodes;  /* paper: 1000                                                   */
+  int32_t check_every;   /* paper: 50                                                     */
+  int32_t eps_every;     /* episodes per epsilon decay step                                       */
+  int32_t reserved;      /* must be 0                                                             */
+  double alpha;          /* Eq. 1 coefficient, >= 0                                               */
+  double lr;             /* learning rate in (0, 1]                                               */
+  double eps0, eps_decay, eps_floor;
+  uint64_t seed;         /* SplitMix64 seed                                                       */
+} ed_rl_config_t;        /* defaults (A-26): SORT, 4, 1000, 50, 10, 0, .5, .1, .5, .95, .02 */
+
+typedef struct ed_fsm_learned_s ed_fsm_learned_t;  /* opaque; owned by the caller */
+
+typedef struct {
+  int64_t episodes;         /* episodes run (early stop included)                               */
+  int64_t table_entries;    /* states with a learned action                                     */
+  int64_t q_entries;        /* (state, action) pairs with a Q value                             */
+  int64_t checkpoints;      /* greedy evaluations run                                           */
+  int64_t final_batches;    /* greedy batch total of the returned table over the instances      */
+  int64_t lower_bound;      /* sum of the instances' App. B.3 lower bounds                      */
+  double learn_us;          /* host time                                                        */
+} ed_fsm_learned_info_t;
+
+/* Learn an FSM table.  Graphs/types as for ed_plan (validated the same way; errors likewise);
+ * ED_E_INVALID_ARG for a bad config. */
+ed_status_t ed_fsm_learn(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_type_t *types,
+                         int32_t num_types, const ed_rl_config_t *cfg, ed_fsm_learned_t **out);
+ed_status_t ed_fsm_learned_info(const ed_fsm_learned_t *fl, ed_fsm_learned_info_t *out);
+/* The learned table as an ed_fsm_t for ed_plan (encoder of the config, fallback key[0]).  The
+ * entries and keys are owned by fl and valid until ed_fsm_learned_destroy. */
+ed_status_t ed_fsm_learned_table(const ed_fsm_learned_t *fl, ed_fsm_t *out);
+/* Q entry k in (state key lexicographic, action ascending) order: key[*key_len] (capacity
+ * num_types), action and value. */
+ed_status_t ed_fsm_learned_q(const ed_fsm_learned_t *fl, int64_t k, int32_t *key, int32_t *key_len,
+                             int32_t *action, double *q);
+/* Checkpoint c: episode count and greedy batch total at that checkpoint. */
+ed_status_t ed_fsm_learned_checkpoint(const ed_fsm_learned_t *fl, int64_t c, int64_t *episode,
+                                      int64_t *batches);
+void ed_fsm_learned_destroy(ed_fsm_learned_t *fl);
+
 /* Version string and build arch, e.g. "ed_batch 0.1 sm_100a". */
 const char *ed_version(void);
 

@@ -19,6 +19,7 @@
 #include "ed_batch.h"
 #include "ed_internal.h"
 #include "ed_layout.h"
+#include "ed_rl.h"
 
 namespace {
 
@@ -588,6 +589,109 @@ static ed_status_t lower(ed_plan_t *pl) {
 extern "C" {
 
 const char *ed_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------------------------------------
+// FSM learning (PAPER §2.3): graphs validated as for ed_plan, split back into instances
+// ------------------------------------------------------------------------------------------------
+struct ed_fsm_learned_s {
+  ed::RlResult res;
+  int32_t encoder = ED_ENC_SORT;
+  std::vector<std::vector<int32_t>> keys;   // table keys (storage for the ed_fsm_t view)
+  std::vector<ed_fsm_entry_t> entries;
+  std::vector<std::pair<std::vector<int32_t>, std::pair<int32_t, double>>> qlist;
+  double learn_us = 0;
+};
+
+ed_status_t ed_fsm_learn(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_type_t *types, int32_t num_types,
+                         const ed_rl_config_t *cfg, ed_fsm_learned_t **out) {
+  const double t0 = now_us();
+  if (!out || !cfg) return fail(ED_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (num_graphs <= 0 || !graphs) return fail(ED_E_INVALID_ARG, "no graphs");
+  if (num_types <= 0 || !types) return fail(ED_E_INVALID_ARG, "bad types");
+  ed_plan_t tmp;
+  tmp.types.assign(types, types + num_types);
+  ed_status_t st = validate_and_merge(&tmp, graphs, num_graphs);
+  if (st != ED_OK) return st;
+  std::vector<ed::RlGraph> gs(num_graphs);
+  int64_t base = 0;
+  for (int gi = 0; gi < num_graphs; ++gi) {
+    ed::RlGraph &g = gs[gi];
+    g.n = graphs[gi].num_nodes;
+    g.type.assign(tmp.gtype.begin() + base, tmp.gtype.begin() + base + g.n);
+    g.pred_off.assign(1, 0);
+    for (int v = 0; v < g.n; ++v) {
+      std::vector<int32_t> pr;
+      for (int k = tmp.in_off[base + v]; k < tmp.in_off[base + v + 1]; ++k)
+        if (tmp.in_idx[k] >= 0) pr.push_back(static_cast<int32_t>(tmp.in_idx[k] - base));
+      std::sort(pr.begin(), pr.end());
+      pr.erase(std::unique(pr.begin(), pr.end()), pr.end());  // distinct dependencies
+      g.preds.insert(g.preds.end(), pr.begin(), pr.end());
+      g.pred_off.push_back(static_cast<int32_t>(g.preds.size()));
+    }
+    base += g.n;
+  }
+  ed_fsm_learned_t *fl = new (std::nothrow) ed_fsm_learned_t();
+  if (!fl) return fail(ED_E_OOM, "out of host memory");
+  if (ed::rl_train(gs, num_types, *cfg, &fl->res) != 0) {
+    delete fl;
+    return fail(ED_E_INVALID_ARG, "bad RL config");
+  }
+  fl->encoder = cfg->encoder;
+  for (const auto &kv : fl->res.table) fl->keys.push_back(kv.first);
+  size_t k = 0;
+  for (const auto &kv : fl->res.table) {
+    fl->entries.push_back(ed_fsm_entry_t{static_cast<int32_t>(fl->keys[k].size()), fl->keys[k].data(), kv.second});
+    ++k;
+  }
+  for (const auto &kv : fl->res.q) fl->qlist.push_back({kv.first.first, {kv.first.second, kv.second}});
+  fl->learn_us = now_us() - t0;
+  *out = fl;
+  return ED_OK;
+}
+
+ed_status_t ed_fsm_learned_info(const ed_fsm_learned_t *fl, ed_fsm_learned_info_t *o) {
+  if (!fl || !o) return fail(ED_E_INVALID_ARG, "null argument");
+  o->episodes = fl->res.episodes;
+  o->table_entries = static_cast<int64_t>(fl->entries.size());
+  o->q_entries = static_cast<int64_t>(fl->qlist.size());
+  o->checkpoints = static_cast<int64_t>(fl->res.checkpoints.size());
+  o->final_batches = fl->res.final_batches;
+  o->lower_bound = fl->res.lower_bound;
+  o->learn_us = fl->learn_us;
+  return ED_OK;
+}
+
+ed_status_t ed_fsm_learned_table(const ed_fsm_learned_t *fl, ed_fsm_t *o) {
+  if (!fl || !o) return fail(ED_E_INVALID_ARG, "null argument");
+  o->encoder = fl->encoder;
+  o->num_entries = static_cast<int32_t>(fl->entries.size());
+  o->entries = fl->entries.empty() ? nullptr : fl->entries.data();
+  o->fallback = ED_FALLBACK_KEY0;
+  return ED_OK;
+}
+
+ed_status_t ed_fsm_learned_q(const ed_fsm_learned_t *fl, int64_t k, int32_t *key, int32_t *key_len, int32_t *action,
+                             double *q) {
+  if (!fl || !key || !key_len || !action || !q) return fail(ED_E_INVALID_ARG, "null argument");
+  if (k < 0 || k >= static_cast<int64_t>(fl->qlist.size())) return fail(ED_E_INVALID_ARG, "entry out of range");
+  const auto &e = fl->qlist[k];
+  std::copy(e.first.begin(), e.first.end(), key);
+  *key_len = static_cast<int32_t>(e.first.size());
+  *action = e.second.first;
+  *q = e.second.second;
+  return ED_OK;
+}
+
+ed_status_t ed_fsm_learned_checkpoint(const ed_fsm_learned_t *fl, int64_t c, int64_t *episode, int64_t *batches) {
+  if (!fl || !episode || !batches) return fail(ED_E_INVALID_ARG, "null argument");
+  if (c < 0 || c >= static_cast<int64_t>(fl->res.checkpoints.size())) return fail(ED_E_INVALID_ARG, "checkpoint out of range");
+  *episode = fl->res.checkpoints[c].first;
+  *batches = fl->res.checkpoints[c].second;
+  return ED_OK;
+}
+
+void ed_fsm_learned_destroy(ed_fsm_learned_t *fl) { delete fl; }
 
 const char *ed_version(void) { return "ed_batch 0.1 sm_100a"; }
 

@@ -82,6 +82,18 @@ class ed_io_t(ctypes.Structure):
     _fields_ = [("out_root", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
 
 
+class ed_rl_config_t(ctypes.Structure):
+    _fields_ = [("encoder", ctypes.c_int32), ("n_steps", ctypes.c_int32), ("max_episodes", ctypes.c_int32),
+                ("check_every", ctypes.c_int32), ("eps_every", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("alpha", ctypes.c_double), ("lr", ctypes.c_double), ("eps0", ctypes.c_double),
+                ("eps_decay", ctypes.c_double), ("eps_floor", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+class ed_fsm_learned_info_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("episodes", "table_entries", "q_entries", "checkpoints",
+                                               "final_batches", "lower_bound")] + [("learn_us", ctypes.c_double)]
+
+
 class EdError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"{STATUS.get(code, code)}: {msg}")
@@ -110,6 +122,17 @@ def _load() -> ctypes.CDLL:
     lib.ed_execute_launch_count.argtypes = [ctypes.c_void_p]
     lib.ed_plan_upload_bytes.argtypes = [ctypes.c_void_p]
     lib.ed_plan_upload_bytes.restype = ctypes.c_int64
+    lib.ed_fsm_learn.argtypes = [_p(ed_graph_t), ctypes.c_int32, _p(ed_op_type_t), ctypes.c_int32,
+                                 _p(ed_rl_config_t), _p(ctypes.c_void_p)]
+    lib.ed_fsm_learned_info.argtypes = [ctypes.c_void_p, _p(ed_fsm_learned_info_t)]
+    lib.ed_fsm_learned_table.argtypes = [ctypes.c_void_p, _p(ed_fsm_t)]
+    lib.ed_fsm_learned_q.argtypes = [ctypes.c_void_p, ctypes.c_int64, _i32p, _i32p, _i32p, _p(ctypes.c_double)]
+    lib.ed_fsm_learned_checkpoint.argtypes = [ctypes.c_void_p, ctypes.c_int64, _p(ctypes.c_int64), _p(ctypes.c_int64)]
+    lib.ed_fsm_learned_destroy.argtypes = [ctypes.c_void_p]
+    lib.ed_fsm_learned_destroy.restype = None
+    for f in ("ed_fsm_learn", "ed_fsm_learned_info", "ed_fsm_learned_table", "ed_fsm_learned_q",
+              "ed_fsm_learned_checkpoint"):
+        getattr(lib, f).restype = ctypes.c_int32
     lib.ed_last_error.restype = ctypes.c_char_p
     lib.ed_version.restype = ctypes.c_char_p
     for f in ("ed_plan", "ed_plan_info", "ed_plan_get_schedule", "ed_plan_get_layout", "ed_plan_get_slot_modes",
@@ -143,6 +166,69 @@ def fsm_from_priority(priority: Sequence[int], num_types: int) -> List[Tuple[Tup
         for key in itertools.permutations(range(num_types), k):
             out.append((key, min(key, key=lambda t: rank.get(t, len(rank) + t))))
     return out
+
+
+def _graph_arrays(graphs, keep):
+    garr = (ed_graph_t * max(len(graphs), 1))()
+    for k, g in enumerate(graphs):
+        arrs = [_i32(g.type), _i32(g.in_off), _i32(g.in_idx) if len(g.in_idx) else _i32([0]), _i32(g.ext)]
+        keep.append(arrs)
+        garr[k] = ed_graph_t(int(len(g.type)), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), int(g.root))
+    return garr
+
+
+def _type_array(types):
+    tarr = (ed_op_type_t * len(types))()
+    for k, t in enumerate(types):
+        tarr[k] = ed_op_type_t(CELL[t.kind], t.num_slots, t.variadic, t.has_ext, t.weight_set, t.hidden,
+                               t.out_dim, DTYPE[t.dtype])
+    return tarr
+
+
+class LearnedFsm:
+    """FSM table learned by ed_fsm_learn (PAPER §2.3): table entries as (key, action), Q values,
+    checkpoints (episode, greedy batch total) and info."""
+
+    def __init__(self, handle, num_types: int):
+        self.handle = handle
+        info = ed_fsm_learned_info_t()
+        _check(LIB.ed_fsm_learned_info(handle, ctypes.byref(info)))
+        self.info = {n: getattr(info, n) for n, _ in ed_fsm_learned_info_t._fields_}
+        f = ed_fsm_t()
+        _check(LIB.ed_fsm_learned_table(handle, ctypes.byref(f)))
+        self.encoder = f.encoder
+        self.table = [(tuple(f.entries[e].key[i] for i in range(f.entries[e].key_len)), f.entries[e].action)
+                      for e in range(f.num_entries)]
+        self.q = {}
+        key = (ctypes.c_int32 * max(num_types, 1))()
+        kl, a, v = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+        for k in range(self.info["q_entries"]):
+            _check(LIB.ed_fsm_learned_q(handle, k, key, ctypes.byref(kl), ctypes.byref(a), ctypes.byref(v)))
+            self.q[(tuple(key[i] for i in range(kl.value)), a.value)] = v.value
+        self.checkpoints = []
+        ep, nb = ctypes.c_int64(), ctypes.c_int64()
+        for c in range(self.info["checkpoints"]):
+            _check(LIB.ed_fsm_learned_checkpoint(handle, c, ctypes.byref(ep), ctypes.byref(nb)))
+            self.checkpoints.append((ep.value, nb.value))
+
+    def __del__(self):
+        if getattr(self, "handle", None) and LIB is not None:
+            LIB.ed_fsm_learned_destroy(self.handle)
+            self.handle = None
+
+
+def ed_fsm_learn(graphs, types, encoder: int = ED_ENC_SORT, alpha: float = 0.5, lr: float = 0.1, eps0: float = 0.5,
+                 eps_decay: float = 0.95, eps_every: int = 10, eps_floor: float = 0.02, n_steps: int = 4,
+                 max_episodes: int = 1000, check_every: int = 50, seed: int = 4000) -> LearnedFsm:
+    """Learn an FSM table by tabular N-step Q-learning (include/ed_batch.h ed_fsm_learn)."""
+    keep = []
+    garr = _graph_arrays(graphs, keep)
+    tarr = _type_array(types)
+    cfg = ed_rl_config_t(encoder, n_steps, max_episodes, check_every, eps_every, 0, alpha, lr, eps0, eps_decay,
+                         eps_floor, seed)
+    h = ctypes.c_void_p()
+    _check(LIB.ed_fsm_learn(garr, len(graphs), tarr, len(types), ctypes.byref(cfg), ctypes.byref(h)))
+    return LearnedFsm(h, len(types))
 
 
 class Plan:

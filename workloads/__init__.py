@@ -424,6 +424,28 @@ def fig1_fixture() -> tuple:
     return b.build(r), ["I", "O", "R"]
 
 
+def b4_fixture() -> tuple:
+    """PAPER App. B.4 "we concatenate two tree networks, but the second has the type of
+    Internal node and Output Node swapped": the Fig. 1 tree (types 0 = I, 1 = O, 2 = R) followed by
+    a second Fig. 1 tree whose spine ops have type O and whose output ops have type I; the second
+    tree's first spine op also reads the first tree's root (the concatenation).  Arities differ
+    between the two halves, so op types for the C ABI must be variadic.  Returns (graph, names)."""
+    b = _GraphBuilder()
+    for half in range(2):
+        spine_t, out_t = (0, 1) if half == 0 else (1, 0)
+        first_in = [-1, -2] if half == 0 else [prev_root, -2]
+        i1 = b.add(spine_t, first_in)
+        i2 = b.add(spine_t, [i1, -3])
+        i3 = b.add(spine_t, [i2, -4])
+        outs = [b.add(out_t, [-1 - k]) for k in range(4)]
+        outs += [b.add(out_t, [i]) for i in (i1, i2, i3)]
+        r = b.add(2, [outs[0], outs[1]])
+        for o in outs[2:]:
+            r = b.add(2, [r, o])
+        prev_root = r
+    return b.build(prev_root), ["I", "O", "R"]
+
+
 def fig3_fixture() -> tuple:
     """PAPER Fig. 3 / §3.1 as a 3-type DAG (SURVEY §8(c) layout pin, A-25).
 
