@@ -51,8 +51,17 @@ def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
     if scaling == "strong":
         from paper_2302_03851_b200.sharding import shard_graphs
         wl = W.config(name)
-        _, wl.graphs = shard_graphs(wl.graphs, rank, world)
+        n_total = len(wl.graphs)
+        wl.shard_idx, wl.graphs = shard_graphs(wl.graphs, rank, world)
+        wl.n_total = n_total
         return wl
+    wl = _weak_workload(name, rank)
+    wl.shard_idx = [rank * len(wl.graphs) + i for i in range(len(wl.graphs))]   # global instance ids
+    wl.n_total = world * len(wl.graphs)
+    return wl
+
+
+def _weak_workload(name: str, rank: int):
     if rank == 0:
         return W.config(name)
     if name in ("cfg3", "cfg3_gru"):
@@ -269,6 +278,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2302_03851_b200 import edbatch as E
+    from paper_2302_03851_b200.sharding import gather_roots
 
     wl = make_workload(args.config, rank, world, args.scaling)
     layout = E.ED_LAYOUT_PQ if args.layout == "pq" else E.ED_LAYOUT_SCHEDULE_ORDER
@@ -290,6 +300,8 @@ def main():
 
     for _ in range(args.warmup):
         E.ed_execute(plan, weights, ws, out)
+        if dist:
+            gather_roots(out, wl.shard_idx, wl.n_total)
     torch.cuda.synchronize()
 
     clocks = ClockSampler()
@@ -304,9 +316,9 @@ def main():
         flush.zero_()                          # untimed: evict L2 between timed steps
         evs[k][0].record(stream)
         E.ed_execute(plan, weights, ws, out)
+        if dist:  # the sharded path's one collective: root rows all-gathered (NCCL / NVLink)
+            gather_roots(out, wl.shard_idx, wl.n_total)
         evs[k][1].record(stream)
-        if k == args.steps - 1:
-            pass
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -333,6 +345,8 @@ def main():
         p2 = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging)   # host scheduling + layout
         ws.plan_info = p2.info
         E.ed_execute(p2, weights, ws, out)                         # uploads the step table (H2D)
+        if dist:
+            gather_roots(out, wl.shard_idx, wl.n_total)
         host_out.copy_(out, non_blocking=True)                     # D2H of the step's result
         b.record(stream)
         torch.cuda.synchronize()

@@ -38,6 +38,11 @@ def _worker(rank, world, port, q):
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         shards = [None] * world
         dist.all_gather_object(shards, idx)
+        # the sharded path's one collective: root outputs gathered into global instance order
+        from paper_2302_03851_b200.sharding import gather_roots
+        local = torch.stack([torch.full((4,), float(i)) for i in idx]) if idx else torch.zeros(0, 4)
+        full = gather_roots(local, idx, len(wl.graphs))
+        assert torch.equal(full[:, 0], torch.arange(len(wl.graphs), dtype=torch.float32))
         if rank == 0:
             q.put((t.tolist(), float(ms.item()), shards, wl.num_nodes, len(wl.graphs)))
     finally:
