@@ -1149,8 +1149,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
       const bool bias_smem = bsrc != nullptr && st.gates * h * 4 <= kBiasBytes;
-      if (bias_smem)
-        for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
+      if (bias_smem) {  // float4 loads issued back to back (G*h/4 <= 640 -> <= 5 per thread)
+        const int n4 = st.gates * h / 4;
+        const float4 *b4 = reinterpret_cast<const float4 *>(bsrc);
+        float4 tmp[5];
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+          if (tid + u * kEpiThreads < n4) tmp[u] = __ldg(b4 + tid + u * kEpiThreads);
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+          if (tid + u * kEpiThreads < n4) reinterpret_cast<float4 *>(sbias)[tid + u * kEpiThreads] = tmp[u];
+      }
       asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
       const float *bias = bias_smem ? sbias : bsrc;
       for (int t = t0; t < T; t += G) {
@@ -1334,6 +1343,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA below
         if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
+        int cb[2] = {-1, -1};  // per K segment: base row of its contiguous block, or -1 (gathered)
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg)
+          if (sg < nseg && !segment_contig(p, st, sg, &cb[sg])) cb[sg] = -1;
         for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
           const int nk = min(kps, kc_total - kc0);
           const uint32_t stg = pipe.it % kStages;
@@ -1354,8 +1367,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           const int kc = kc0;
           const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
           uint8_t *a_dst = stages + stg * kStageBytes;
-          int cbase = -1;
-          if (segment_contig(p, st, seg, &cbase)) {
+          const int cbase = seg == 0 ? cb[0] : cb[1];
+          if (cbase >= 0) {
             if (lt == 0) {
               mbar_arrive_tx(full + stg, kAStage);
               if (st.cell == kCellMvP)  // U rows: [B a | A b], 2h columns
