@@ -167,7 +167,11 @@ inline int cell_segments(int cell) {
 
 // Readiness units a device step publishes per row of its output block when it completes: h for
 // row-vector results; h * h (elements) for the MV-RNN matrix product.
-inline int step_contrib(int cell, int h) { return cell == kCellMvMat ? h * h : h; }
+// Output-linear ops (logits in Y, A-7) are sinks: nothing waits for them, so they publish nothing.
+inline int step_contrib(int cell, int h) {
+  if (cell == ED_CELL_LINEAR_OUT || cell == kCellTaggerOut) return 0;
+  return cell == kCellMvMat ? h * h : h;
+}
 
 // Launch entry points implemented in ed_kernels.cu (return cudaError_t as int).
 int launch_persistent(const KParams &p, int dtype, int grid, void *stream);

@@ -212,6 +212,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // step_contrib over the device steps that write it (h per row-vector result, h*h for a matrix).  A consumer acquires ready[row] >= target[row] before reading
 // the row; a producer publishes with a release-add after its stores.  Rows are only produced by
 // earlier device steps and every warp walks the steps in order, so waiting cannot deadlock.
+__device__ __forceinline__ int ld_relaxed_s32(const int *a) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ int ld_acquire_s32(const int *a) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
@@ -225,7 +230,11 @@ __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep 
   if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
   if (need <= 0) return;
   unsigned spins = 0;
+#ifdef ED_RELAXED_POLL
+  while (ld_relaxed_s32(p.ready + e) < need) {
+#else
   while (ld_acquire_s32(p.ready + e) < need) {
+#endif
     if (++spins > (1u << 26)) {  // watchdog: report the stuck dependency, then abort the launch
       printf("ed_batch watchdog: block %d thread %d cell %d out_row0 %d row %d ready %d need %d\n", blockIdx.x,
              threadIdx.x, st.cell, st.out_row0, e, ld_acquire_s32(p.ready + e), need);
@@ -239,7 +248,11 @@ __device__ __forceinline__ bool row_ready(const KParams &p, int e, const DevStep
   if (e < 0 || e >= p.rows) return true;
   int need = __ldg(p.target + e);
   if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
+#ifdef ED_RELAXED_POLL
+  return need <= 0 || ld_relaxed_s32(p.ready + e) >= need;
+#else
   return need <= 0 || ld_acquire_s32(p.ready + e) >= need;
+#endif
 }
 __device__ __forceinline__ void publish_row(const KParams &p, int row, int units) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + row), "r"(units) : "memory");
@@ -527,8 +540,7 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
     }
     if (lane == 0) {
       float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
-      publish_row(p, st.out_row0 + static_cast<int>(i), h);
+      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];  // sink: no readiness to publish
     }
   }
 }
@@ -584,6 +596,7 @@ __device__ void linear_out_rows_bf16(const KParams &p, const DevStep &st, long i
     }
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
+      if (c >= C) break;  // warp-uniform
       float x = acc[c];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -592,8 +605,7 @@ __device__ void linear_out_rows_bf16(const KParams &p, const DevStep &st, long i
     const long i = i0 + r;
     if (lane == 0 && i < st.m) {
       float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];
-      publish_row(p, st.out_row0 + static_cast<int>(i), h);
+      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];  // sink: no readiness to publish
     }
   }
 }
@@ -1129,13 +1141,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
       const int C = st.gates;
       const bool in_smem = C * h * 4 <= kWoutBytes;
-      if (in_smem) {
-        const float *W = static_cast<const float *>(step_W(p, st));
-        for (int q = tid; q < C * h; q += kThreadsTC) swout[q] = W[q];
+      if (in_smem) {  // float4 loads issued back to back (C*h/4 <= 768 -> <= 2 per thread)
+        const float4 *W4 = static_cast<const float4 *>(step_W(p, st));
+        const int n4 = C * h / 4;
+        float4 tmp[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (tid + u * kThreadsTC < n4) tmp[u] = __ldg(W4 + tid + u * kThreadsTC);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (tid + u * kThreadsTC < n4) reinterpret_cast<float4 *>(swout)[tid + u * kThreadsTC] = tmp[u];
       }
+      if (p.trace && tid == 0) p.trace[p.num_steps * 64 + blockIdx.x * 4 + 0] = globaltimer();
       __syncthreads();
+      if (p.trace && tid == 0) p.trace[p.num_steps * 64 + blockIdx.x * 4 + 1] = globaltimer();
       const float *Ws = in_smem ? swout : static_cast<const float *>(step_W(p, st));
       for (int t = t0; t < T; t += G) linear_out_rows_bf16(p, st, static_cast<long>(t) * kSimtRows + 2 * warp, Ws);
+      if (p.trace && lane == 0) atomicMax(p.trace + p.num_steps * 64 + blockIdx.x * 4 + 2, globaltimer());
       __syncthreads();  // swout is reused by the next SIMT step
       if (tid == 0) stamp_step(p, s);
       continue;

@@ -10,12 +10,14 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 wl = W.config(name)
 plan, w, ws, out = run_gpu(wl)
 nb = plan.info["num_steps"]
-tr = torch.zeros(nb * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(nb * 64 + 148 * 4, dtype=torch.int64, device="cuda")
 for _ in range(3):
     tr.zero_()
     E.ed_execute(plan, w, ws, out, trace=tr)
 torch.cuda.synchronize()
-t = tr.view(nb, 64).cpu().numpy().astype(np.int64)
+full = tr.cpu().numpy().astype(np.int64)
+t = full[:nb * 64].reshape(nb, 64)
+pc = full[nb * 64:].reshape(148, 4)
 i = ws.plan_info
 ts = ws._view(i["off_ts"], nb + 1, torch.int64).cpu().numpy().astype(np.int64)
 end = np.maximum.accumulate(ts)
@@ -25,3 +27,10 @@ for s in range(nb):
     base = end[s]
     rel = lambda k: int(t[s, k] - base) if t[s, k] else None
     print(s, len(sched[min(s, len(sched) - 1)][1]), [rel(k) for k in (0, 1, 2, 3, 4, 6, 5)], "|", int(ts[s + 1] - base))
+
+# per-CTA SIMT (last step) phases: entered, passed the CTA barrier, items done (rel. to previous step end)
+base = end[nb - 1]
+rows = [(c, int(pc[c, 0] - base), int(pc[c, 1] - base), int(pc[c, 2] - base)) for c in range(148) if pc[c, 0]]
+rows.sort(key=lambda r: -r[3])
+print("last step per CTA (cta, enter, synced, done) slowest first:", rows[:12])
+print("median enter/synced/done:", [int(np.median([r[k] for r in rows])) for k in (1, 2, 3)])
