@@ -160,6 +160,8 @@ typedef struct {
                               /*   blocks by their producers' epilogues (read as TMA boxes)     */
   int64_t staged_bytes;       /* bytes of those extra producer stores per execute               */
   int64_t h_rows;             /* rows of the H buffer: num_rows + staged operand rows           */
+  double validate_us;         /* host time of validation + merge (part of plan_us)              */
+  double lower_us;            /* host time of lowering (step table, index arrays, workspace map) */
 } ed_plan_info_t;
 
 /* Per weight set, device pointers.  Matrices must have been packed by ed_pack_weights.

@@ -18,7 +18,7 @@ BUILD = os.path.join(PKG, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INC, "-I" + CSRC]
-CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I" + INC, "-I" + CSRC, "-I/usr/local/cuda/include", "-Wall"]
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I" + INC, "-I" + CSRC, "-I/usr/local/cuda/include", "-Wall"]
 
 SOURCES = ["ed_batch.cpp", "ed_layout.cpp", "ed_rl.cpp", "ed_kernels.cu"]
 

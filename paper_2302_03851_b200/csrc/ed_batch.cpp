@@ -152,7 +152,7 @@ struct ed_plan_s {
   int64_t op_rows = 0;      // staged operand rows appended to H (rows V+1 ..)
   int64_t staged = 0, staged_bytes = 0;
   int64_t dst_base = 0;     // idx offset of dst_off[V + 2] (then the copy destinations)
-  double plan_us = 0, sched_us = 0, layout_us = 0;
+  double plan_us = 0, sched_us = 0, layout_us = 0, validate_us = 0, lower_us = 0;
   // upload state
   std::vector<uint8_t> blob;          // [ts zeros | steps | idx | roots]
   int grid = 0;
@@ -775,7 +775,9 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   if (st != ED_OK) { delete pl; return st; }
   pl->sched_us = t2 - t1;
   pl->layout_us = t3 - t2;
+  pl->validate_us = t1 - t0;
   pl->plan_us = now_us() - t0;
+  pl->lower_us = pl->plan_us - (t3 - t0);
   *out = pl;
   return ED_OK;
 }
@@ -809,6 +811,8 @@ ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
   o->plan_us = pl->plan_us;
   o->schedule_us = pl->sched_us;
   o->layout_us = pl->layout_us;
+  o->validate_us = pl->validate_us;
+  o->lower_us = pl->lower_us;
   o->staged_operands = pl->staged;
   o->staged_bytes = pl->staged_bytes;
   o->h_rows = pl->V + 1 + pl->op_rows;

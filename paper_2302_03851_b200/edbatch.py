@@ -65,7 +65,8 @@ _INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bo
 class ed_plan_info_t(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in _INFO_I64] + [
         ("plan_us", ctypes.c_double), ("schedule_us", ctypes.c_double), ("layout_us", ctypes.c_double),
-        ("staged_operands", ctypes.c_int64), ("staged_bytes", ctypes.c_int64), ("h_rows", ctypes.c_int64)]
+        ("staged_operands", ctypes.c_int64), ("staged_bytes", ctypes.c_int64), ("h_rows", ctypes.c_int64),
+        ("validate_us", ctypes.c_double), ("lower_us", ctypes.c_double)]
 
 
 class ed_weight_set_t(ctypes.Structure):
@@ -168,13 +169,36 @@ def fsm_from_priority(priority: Sequence[int], num_types: int) -> List[Tuple[Tup
     return out
 
 
+# ed_graph_t as a numpy record (x86-64 layout: int32, pad, 4 pointers, int32, pad = 48 bytes), so
+# that a minibatch of thousands of graphs is marshalled with a few vectorized numpy operations
+_GRAPH_REC = np.dtype([("num_nodes", np.int32), ("_p0", np.int32), ("type", np.uint64), ("in_off", np.uint64),
+                       ("in_idx", np.uint64), ("ext", np.uint64), ("root", np.int32), ("_p1", np.int32)])
+assert _GRAPH_REC.itemsize == ctypes.sizeof(ed_graph_t)
+
+
 def _graph_arrays(graphs, keep):
-    garr = (ed_graph_t * max(len(graphs), 1))()
-    for k, g in enumerate(graphs):
-        arrs = [_i32(g.type), _i32(g.in_off), _i32(g.in_idx) if len(g.in_idx) else _i32([0]), _i32(g.ext)]
-        keep.append(arrs)
-        garr[k] = ed_graph_t(int(len(g.type)), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), int(g.root))
-    return garr
+    """ed_graph_t[len(graphs)] pointing into four concatenated int32 arrays (kept alive in keep)."""
+    n = len(graphs)
+    sizes = np.fromiter((len(g.type) for g in graphs), dtype=np.int64, count=n)
+    nin = np.fromiter((len(g.in_idx) for g in graphs), dtype=np.int64, count=n)
+    cat = lambda xs: np.ascontiguousarray(np.concatenate(xs).astype(np.int32, copy=False)) if n else np.zeros(1, np.int32)
+    types = cat([g.type for g in graphs])
+    offs = cat([g.in_off for g in graphs])
+    idx = cat([g.in_idx for g in graphs] + [np.zeros(1, np.int32)])
+    ext = cat([g.ext for g in graphs])
+    keep.append((types, offs, idx, ext))
+    node_off = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if n else np.zeros(0, np.int64)
+    in_off_off = node_off + np.arange(n)                   # each in_off has num_nodes + 1 entries
+    idx_off = np.concatenate([[0], np.cumsum(nin)[:-1]]) if n else np.zeros(0, np.int64)
+    rec = np.zeros(max(n, 1), dtype=_GRAPH_REC)
+    rec["num_nodes"][:n] = sizes
+    rec["type"][:n] = types.ctypes.data + 4 * node_off
+    rec["in_off"][:n] = offs.ctypes.data + 4 * in_off_off
+    rec["in_idx"][:n] = idx.ctypes.data + 4 * idx_off
+    rec["ext"][:n] = ext.ctypes.data + 4 * node_off
+    rec["root"][:n] = np.fromiter((int(g.root) for g in graphs), dtype=np.int32, count=n)
+    keep.append(rec)
+    return rec.ctypes.data_as(_p(ed_graph_t))
 
 
 def _type_array(types):
@@ -276,15 +300,8 @@ def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: in
     """graphs: objects with numpy fields type/in_off/in_idx/ext and int root (workloads.Graph);
     types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype."""
     keep = []
-    garr = (ed_graph_t * max(len(graphs), 1))()
-    for k, g in enumerate(graphs):
-        arrs = [_i32(g.type), _i32(g.in_off), _i32(g.in_idx) if len(g.in_idx) else _i32([0]), _i32(g.ext)]
-        keep.append(arrs)
-        garr[k] = ed_graph_t(int(len(g.type)), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), int(g.root))
-    tarr = (ed_op_type_t * len(types))()
-    for k, t in enumerate(types):
-        tarr[k] = ed_op_type_t(CELL[t.kind], t.num_slots, t.variadic, t.has_ext, t.weight_set, t.hidden,
-                               t.out_dim, DTYPE[t.dtype])
+    garr = _graph_arrays(graphs, keep)
+    tarr = _type_array(types)
     earr = (ed_fsm_entry_t * max(len(fsm), 1))()
     for k, (key, act) in enumerate(fsm):
         ka = _i32(list(key))
