@@ -29,6 +29,7 @@ import workloads as W  # noqa: E402
 METRIC = "instances/sec TreeLSTM h=512 (BASELINE cfg3: 256 random trees, bf16) per step, whole job"
 METRICS = {"cfg3": METRIC,
            "cfg3_gru": "instances/sec TreeGRU h=512 (256 random trees, bf16) per step, whole job",
+           "cfg3_2type": "instances/sec TreeLSTM-2Type h=512 (256 random trees, bf16) per step, whole job",
            "cfg1": "instances/sec TreeLSTM h=32 (cfg1: 8 random trees, fp32) per step, whole job",
            "cfg2": "instances/sec BiLSTM-tagger h=256 (cfg2: 64 sequences, bf16) per step, whole job",
            "cfg5": "instances/sec LatticeLSTM h=256 (cfg5: 512 lattices, bf16) per step, whole job",
@@ -37,6 +38,7 @@ METRICS = {"cfg3": METRIC,
 CONFIGS = {
     "cfg3": "cfg3 TreeLSTM h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
     "cfg3_gru": "cfg3 TreeGRU h=512, 256 parse-like random binary trees (leaves U[5,40]), bf16",
+    "cfg3_2type": "cfg3 TreeLSTM-2Type h=512 (two internal types 50/50, P:291), 256 random trees (leaves U[5,40]), bf16",
     "cfg1": "cfg1 TreeLSTM h=32, 8 random trees (leaves U[2,16]), fp32",
     "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16",
     "cfg5": "cfg5 LatticeLSTM h=256, 512 character lattices (chars U[10,50], word p=0.3), bf16",
@@ -64,6 +66,8 @@ def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
 def _weak_workload(name: str, rank: int):
     if rank == 0:
         return W.config(name)
+    if name == "cfg3_2type":
+        return W.treelstm_2type(256, (5, 40), 512, "bf16", 3 + 100 * rank)
     if name in ("cfg3", "cfg3_gru"):
         return W.treelstm(256, (5, 40), 512, "bf16", 3 + 100 * rank, cell="treegru" if name == "cfg3_gru" else "treelstm")
     if name == "cfg1":

@@ -20,10 +20,11 @@ def rel_err(y: np.ndarray, r: np.ndarray) -> float:
     return float(np.max(np.abs(y - r)) / max(float(np.max(np.abs(r))), 1e-6)) if r.size else 0.0
 
 
-def run_gpu(wl, layout=0, priority=None, stream=None):
+def run_gpu(wl, layout=0, priority=None, stream=None, staging=0, fsm=None):
     from paper_2302_03851_b200 import edbatch as E
     pr = wl.priority if priority is None else priority
-    plan = E.ed_plan(wl.graphs, wl.types, E.fsm_from_priority(pr, len(wl.types)), layout=layout)
+    table = fsm if fsm is not None else E.fsm_from_priority(pr, len(wl.types))
+    plan = E.ed_plan(wl.graphs, wl.types, table, layout=layout, staging=staging)
     w = E.DeviceWeights(wl.types, wl.params)
     ws = E.Workspace(plan)
     dt = torch.bfloat16 if wl.dtype == "bf16" else torch.float32

@@ -140,6 +140,7 @@ CASES = [
     ("bilstm", lambda: W.bilstm(6, (3, 9), 32, "fp32"), dict(max_episodes=150, check_every=50, n_steps=2)),
     ("lattice_base", lambda: W.lattice(8, (6, 12), 32, "fp32"), dict(encoder="base", max_episodes=120,
                                                                       check_every=30)),
+    ("treelstm_2type", lambda: W.treelstm_2type(10, (3, 14), 32, "fp32", cfg=7), dict(max_episodes=200)),
 ]
 
 
@@ -182,3 +183,19 @@ def test_c_learner_rejects_bad_config():
     assert e.value.name == "ED_E_INVALID_ARG"
     with pytest.raises(E.EdError):
         E.ed_fsm_learn(wl.graphs, wl.types, lr=0.0)
+
+
+def test_two_internal_types_learned_beats_priority_and_heuristics():
+    """TreeLSTM-2Type (Table 1): a fixed type priority batches the two internal types apart
+    and needs many more batches; the learned FSM is within a few batches of the lower bound and no
+    worse than the depth / agenda heuristics (Fig. 8)."""
+    from oracle.schedule import table_from_priority
+    wl = W.treelstm_2type(16, (5, 20), 32, "fp32", cfg=7)
+    ms = instances(wl)
+    r = train(ms, RLConfig())
+    learned = sum(len(fsm_schedule(m, r.table)) for m in ms)
+    prio = sum(len(fsm_schedule(m, table_from_priority(wl.priority, 4))) for m in ms)
+    depth = sum(len(depth_schedule(m)) for m in ms)
+    agenda = sum(len(run_alg1(m, agenda_chooser(m))) for m in ms)
+    assert r.lower_bound <= learned <= min(prio, depth, agenda)
+    assert learned < prio

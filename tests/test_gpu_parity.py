@@ -164,3 +164,35 @@ def test_pq_layout_parity_and_bitwise_layout_invariance(wlf):
 
 def test_cfg2_pq_layout_full_size():
     _check(W.config("cfg2"), layout=1)
+
+
+@pytest.mark.parametrize("wlf", [
+    lambda: W.treelstm(60, (1, 40), 128, "bf16", cfg=65),
+    lambda: W.lattice(160, (1, 30), 128, "bf16", cfg=66),
+    lambda: W.bilstm(150, (1, 12), 64, "bf16", cfg=67),
+])
+def test_staged_operands_are_bitwise_invisible(wlf):
+    """Staging (S-1) only changes where the loaders read an operand from: every node record
+    and root is bit-identical with and without it (and matches the oracle)."""
+    wl = wlf()
+    plan_a, _, ws_a, out_a, _ = _check(wl)
+    assert plan_a.info["staged_operands"] > 0
+    plan_b, _, ws_b, out_b = run_gpu(wl, staging=1)
+    assert plan_b.info["staged_operands"] == 0
+    for x, y in zip(_node_records(plan_a, ws_a), _node_records(plan_b, ws_b)):
+        if x is not None:
+            assert np.array_equal(x, y)
+    assert torch.equal(out_a, out_b)
+
+
+def test_treelstm_2type_with_learned_fsm():
+    """TreeLSTM-2Type (Table 1) planned with the Q-learned FSM (paper §2.3): two internal types
+    with separate weight sets in one persistent launch; parity with the oracle."""
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.treelstm_2type(48, (1, 30), 128, "bf16", cfg=68)
+    learned = E.ed_fsm_learn(wl.graphs, wl.types)
+    plan, w, ws, out = run_gpu(wl, fsm=learned.table)
+    err = compare(wl, plan, ws, out)
+    assert all(v <= TOL[wl.dtype] for v in err.values()), err
+    prio = E.ed_plan(wl.graphs, wl.types, E.fsm_from_priority(wl.priority, len(wl.types)))
+    assert plan.info["num_batches"] <= prio.info["num_batches"]

@@ -130,12 +130,14 @@ def graph_from_lists(types: Sequence[int], inputs: Sequence[Sequence[int]],
 # ----------------------------------------------------------------------------------------------
 
 def tree_graph(n_leaves: int, rng: SplitMix64, tok: SplitMix64, vocab: int,
-               t_leaf: Optional[int], t_int: int, t_out: Optional[int]) -> Graph:
+               t_leaf: Optional[int], t_int: int, t_out: Optional[int], t_int2: Optional[int] = None) -> Graph:
     """Tree(n): uniform split point k ~ U[1, n-1]; nodes numbered in post-order.
 
     t_leaf is None -> leaves are external lookups (TreeFC / MV-RNN, SURVEY A-6): internal
     nodes reference them as external ids (-1 - word).  t_out not None -> one output op O
-    per L/I node, appended after all tree nodes in node order (SURVEY A-7).
+    per L/I node, appended after all tree nodes in node order (SURVEY A-7).  t_int2 not None ->
+    TreeLSTM-2Type (Table 1): each internal node is t_int or t_int2 with probability 1/2
+    (one SplitMix64 draw after its children are built).
     """
     b = _GraphBuilder()
 
@@ -148,7 +150,8 @@ def tree_graph(n_leaves: int, rng: SplitMix64, tok: SplitMix64, vocab: int,
         k = rng.randint(1, n - 1)
         left = build(k)
         right = build(n - k)
-        return b.add(t_int, [left, right])
+        t = t_int if t_int2 is None or rng.next_u64() % 2 == 0 else t_int2
+        return b.add(t, [left, right])
 
     root = build(n_leaves)
     if t_out is not None:
@@ -323,6 +326,26 @@ def treelstm(n_trees: int, leaves: tuple, h: int, dtype: str, cfg: int, vocab: i
                     config={"instances": n_trees, "leaves": list(leaves), "cfg": cfg})
 
 
+def treelstm_2type(n_trees: int, leaves: tuple, h: int, dtype: str, cfg: int, vocab: int = 10000,
+                   out_dim: int = 5) -> Workload:
+    """TreeLSTM-2Type (Table 1): "an extension to TreeLSTM that contains two types of internal
+    nodes, each with 50% probability": types L, I1, I2 (same cell, separate weights), O."""
+    rng = SplitMix64(1000 + cfg)
+    tok = SplitMix64(3000 + cfg)
+    types = [OpType("L", "treelstm_leaf", 0, has_ext=1, weight_set=0, hidden=h, dtype=dtype),
+             OpType("I1", "treelstm_internal", 2, weight_set=1, hidden=h, dtype=dtype),
+             OpType("I2", "treelstm_internal", 2, weight_set=2, hidden=h, dtype=dtype),
+             OpType("O", "linear_out", 1, weight_set=3, hidden=h, out_dim=out_dim, dtype=dtype)]
+    graphs = [tree_graph(rng.randint(leaves[0], leaves[1]), rng, tok, vocab, 0, 1, 3, t_int2=2)
+              for _ in range(n_trees)]
+    gen = np.random.default_rng(2000 + cfg)
+    params = [make_params("treelstm_leaf", h, gen, vocab=vocab), make_params("treelstm_internal", h, gen),
+              make_params("treelstm_internal", h, gen), make_params("linear_out", h, gen, out_dim=out_dim)]
+    return Workload(name=f"treelstm2type_h{h}_{dtype}", types=types, graphs=graphs, priority=[0, 1, 2, 3],
+                    params=_finish_params(params, dtype), dtype=dtype, hidden=h,
+                    config={"instances": n_trees, "leaves": list(leaves), "cfg": cfg})
+
+
 def treefc(n_trees: int, leaves: tuple, h: int, dtype: str, cfg: int, vocab: int = 1024,
            cell: str = "treefc") -> Workload:
     """TreeFC / MV-RNN forests: a single internal type; leaves are external lookups (A-6)."""
@@ -389,6 +412,8 @@ def config(name: str) -> Workload:
         return treelstm(256, (5, 40), 512, "bf16", 3)
     if name == "cfg3_gru":
         return treelstm(256, (5, 40), 512, "bf16", 3, cell="treegru")
+    if name == "cfg3_2type":
+        return treelstm_2type(256, (5, 40), 512, "bf16", 3)
     if name == "cfg4_treefc":
         return treefc(1024, (5, 40), 512, "bf16", 4)
     if name == "cfg4_mvrnn":
