@@ -33,6 +33,7 @@ METRICS = {"cfg3": METRIC,
            "cfg1": "instances/sec TreeLSTM h=32 (cfg1: 8 random trees, fp32) per step, whole job",
            "cfg2": "instances/sec BiLSTM-tagger h=256 (cfg2: 64 sequences, bf16) per step, whole job",
            "cfg5": "instances/sec LatticeLSTM h=256 (cfg5: 512 lattices, bf16) per step, whole job",
+           "cfg5_gru": "instances/sec LatticeGRU h=256 (512 lattices, bf16) per step, whole job",
            "cfg4_treefc": "instances/sec TreeFC h=512 (cfg4: 1024 trees, bf16) per step, whole job",
            "cfg4_mvrnn": "instances/sec MV-RNN h=512 (cfg4: 1024 trees, bf16) per step, whole job"}
 CONFIGS = {
@@ -42,6 +43,7 @@ CONFIGS = {
     "cfg1": "cfg1 TreeLSTM h=32, 8 random trees (leaves U[2,16]), fp32",
     "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16",
     "cfg5": "cfg5 LatticeLSTM h=256, 512 character lattices (chars U[10,50], word p=0.3), bf16",
+    "cfg5_gru": "cfg5 LatticeGRU h=256 (P:294, A-27), 512 character lattices (chars U[10,50], word p=0.3), bf16",
     "cfg4_treefc": "cfg4 TreeFC h=512, 1024 random trees (leaves U[5,40]), bf16",
     "cfg4_mvrnn": "cfg4 MV-RNN h=512, 1024 random trees (leaves U[5,40], 1024 word vectors + matrices), bf16",
 }
@@ -76,6 +78,8 @@ def _weak_workload(name: str, rank: int):
         return W.bilstm(64, (10, 50), 256, "bf16", 2 + 100 * rank)
     if name == "cfg5":
         return W.lattice(512, (10, 50), 256, "bf16", 5 + 100 * rank)
+    if name == "cfg5_gru":
+        return W.lattice(512, (10, 50), 256, "bf16", 5 + 100 * rank, cell="latticegru")
     if name == "cfg4_treefc":
         return W.treefc(1024, (5, 40), 512, "bf16", 4 + 100 * rank)
     if name == "cfg4_mvrnn":
@@ -118,12 +122,15 @@ def step_work(kind: str, m: int, h: int, C: int, elt: int):
         return 2 * m * 2 * h * 4 * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h)
     if kind == "lattice_word":
         return 2 * m * 2 * h * 3 * h + 2 * m * 2 * h * h, m * (elt * h + 4 + elt * h + 4 * h + elt * h + 4 * h + 4 * h)
+    if kind in ("latticegru_char", "latticegru_word"):  # GRU over [x; h]: [r; z; n_x; n_h] (A-27)
+        return 2 * m * 2 * h * 4 * h, m * (elt * h + 4 + elt * h + elt * h)
     raise KeyError(kind)
 
 
 def weight_bytes(kind: str, h: int, C: int, elt: int) -> int:
     g = {"treelstm_leaf": (3, 1), "treelstm_internal": (5, 2), "treegru_leaf": (2, 1), "treegru_internal": (5, 2),
-         "treefc_internal": (1, 2), "lstm": (4, 2), "tagger": (1, 2), "lattice_char": (4, 2), "lattice_word": (4, 2)}
+         "treefc_internal": (1, 2), "lstm": (4, 2), "tagger": (1, 2), "lattice_char": (4, 2), "lattice_word": (4, 2),
+         "latticegru_char": (4, 2), "latticegru_word": (4, 2)}
     if kind == "linear_out":
         return 4 * C * h
     if kind == "tagger":

@@ -60,6 +60,10 @@ typedef int32_t ed_status_t;
 #define ED_CELL_MVRNN_INTERNAL     9  /* MV-RNN (Table 4)                            */
 #define ED_CELL_LATTICE_CHAR      10  /* LatticeLSTM char cell (Fig. 7), variadic    */
 #define ED_CELL_LATTICE_WORD      11  /* LatticeLSTM word cell                                     */
+#define ED_CELL_LATTICEGRU_CHAR   12  /* LatticeGRU char cell (A-27): GRU over      */
+                                      /* [x_e; h_{e-1}], max-pooled with the words ending at e      */
+#define ED_CELL_LATTICEGRU_WORD   13  /* LatticeGRU word cell: GRU over [x_w; h_b] (slot: C_b)      */
+#define ED_CELL_MAX               13
 
 #define ED_FP32 0
 #define ED_BF16 1

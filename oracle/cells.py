@@ -128,3 +128,30 @@ def lattice_char(p, x, hp, cp, words):
         for (cw, _), el in zip(words, els):
             c = c + (el / den) * cw
     return sigmoid(o) * np.tanh(c), c
+
+
+# LatticeGRU (A-27) ----------------------------------------------------------------
+
+def gru(p, x, hp):
+    """GRU update in torch.nn.GRUCell form with the weights stacked as one [4h, 2h] matrix over
+    [x; h_prev]: rows [r; z; n_x; n_h] where the n_x rows read x only and the n_h rows h only:
+    r = s(.), z = s(.), n = tanh(n_x + r * n_h), h = (1 - z) * n + z * h_prev."""
+    h = x.shape[0]
+    g = _f64(p, "W") @ np.concatenate([x, hp]) + _f64(p, "b")
+    r, z = sigmoid(g[:h]), sigmoid(g[h:2 * h])
+    n = np.tanh(g[2 * h:3 * h] + r * g[3 * h:])
+    return (1.0 - z) * n + z * hp
+
+
+def latticegru_word(p, xw, hb):
+    """Word cell w = (b -> e): the GRU over (x_w, h_b)."""
+    return gru(p, xw, hb)
+
+
+def latticegru_char(p, x, hp, word_hs):
+    """Char cell e: the GRU over (x_e, h_{e-1}), element-wise max-pooled with the states of the
+    words ending at e (A-27)."""
+    hc = gru(p, x, hp)
+    for hw in word_hs:
+        hc = np.maximum(hc, hw)
+    return hc

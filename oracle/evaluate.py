@@ -78,6 +78,11 @@ def eval_node(wl, t: int, ins: List[dict], ext: int) -> dict:
         x = np.asarray(p["emb"][ext], np.float64)
         words = [(w["c"], w["l"]) for w in ins[1:]]
         rec["h"], rec["c"] = cells.lattice_char(p, x, ins[0]["h"], ins[0]["c"], words)
+    elif k == "latticegru_word":
+        rec["h"] = cells.latticegru_word(p, np.asarray(p["emb"][ext], np.float64), ins[0]["h"])
+    elif k == "latticegru_char":
+        x = np.asarray(p["emb"][ext], np.float64)
+        rec["h"] = cells.latticegru_char(p, x, ins[0]["h"], [w["h"] for w in ins[1:]])
     else:
         raise ValueError(k)
     return rec
@@ -244,6 +249,16 @@ def evaluate_levels(wl) -> List[Dict[int, dict]]:
                     den = num_e + sum(np.exp(Lk[w]) for w in ws)
                     c[r] = num_e / den * tg[r] + sum(np.exp(Lk[w]) / den * C[w] for w in ws)
             hh = so * np.tanh(c)
+        elif k in ("latticegru_word", "latticegru_char"):
+            HP = rows(vs, 0, "h", t)
+            Z = np.concatenate([X, HP], axis=1) @ p["W"].T + p["b"]
+            r_, z_ = _sig(Z[:, :h]), _sig(Z[:, h:2 * h])
+            hh = (1.0 - z_) * np.tanh(Z[:, 2 * h:3 * h] + r_ * Z[:, 3 * h:]) + z_ * HP; c = None
+            if k == "latticegru_char":
+                for r, v in enumerate(vs):
+                    for kk, x in m.inputs[v][1:]:
+                        if kk == "n":
+                            hh[r] = np.maximum(hh[r], H[x])
         else:
             raise ValueError(k)
         H.update(zip(vs, hh))

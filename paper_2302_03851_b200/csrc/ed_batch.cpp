@@ -718,7 +718,7 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   for (int t = 0; t < num_types; ++t) {
     const ed_op_type_t &ot = types[t];
     const std::string tag = "type " + std::to_string(t);
-    if (ot.cell_kind < ED_CELL_TREELSTM_LEAF || ot.cell_kind > ED_CELL_LATTICE_WORD) { delete pl; return fail(ED_E_TYPE, tag + ": unknown cell kind"); }
+    if (ot.cell_kind < ED_CELL_TREELSTM_LEAF || ot.cell_kind > ED_CELL_MAX) { delete pl; return fail(ED_E_TYPE, tag + ": unknown cell kind"); }
     if (ot.hidden != pl->hidden || ot.dtype != pl->dtype) { delete pl; return fail(ED_E_TYPE, tag + ": hidden/dtype differ between types"); }
     if (ot.hidden <= 0) { delete pl; return fail(ED_E_TYPE, tag + ": hidden must be > 0"); }
     if (ot.dtype != ED_BF16 && ot.dtype != ED_FP32) { delete pl; return fail(ED_E_TYPE, tag + ": unknown dtype"); }
@@ -857,7 +857,7 @@ int64_t ed_packed_bytes(int32_t cell_kind, int32_t hidden, int32_t out_dim, int3
 ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which,
                             const float *logical_dev, void *packed_dev, void *stream) {
   if (!logical_dev || !packed_dev) return fail(ED_E_INVALID_ARG, "null pointer");
-  if (cell_kind < ED_CELL_TREELSTM_LEAF || cell_kind > ED_CELL_LATTICE_WORD) return fail(ED_E_TYPE, "unknown cell kind");
+  if (cell_kind < ED_CELL_TREELSTM_LEAF || cell_kind > ED_CELL_MAX) return fail(ED_E_TYPE, "unknown cell kind");
   int sms = 0, major = 0, minor = 0;
   int e = ed::device_check(&sms, &major, &minor);
   if (e) return fail(ED_E_CUDA, std::string("cuda: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));

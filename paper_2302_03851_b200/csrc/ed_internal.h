@@ -107,6 +107,8 @@ inline int cell_gates(int cell) {
     case ED_CELL_LSTM: return 4;
     case ED_CELL_LATTICE_CHAR: return 4;
     case ED_CELL_LATTICE_WORD: return 3;
+    case ED_CELL_LATTICEGRU_CHAR:
+    case ED_CELL_LATTICEGRU_WORD: return 4;  // [r; z; n_x; n_h] (n_x: x part only, n_h: h part only)
     case ED_CELL_TAGGER: return 1;
     case ED_CELL_MVRNN_INTERNAL: return 1;
     case kCellLatticeLink: return 1;
@@ -129,6 +131,8 @@ inline int cell_units(int cell) {
     case ED_CELL_LSTM: return 64;               // N = 256
     case ED_CELL_LATTICE_CHAR: return 64;       // N = 256
     case ED_CELL_LATTICE_WORD: return 80;       // N = 240
+    case ED_CELL_LATTICEGRU_CHAR:
+    case ED_CELL_LATTICEGRU_WORD: return 64;    // N = 256
     case kCellLatticeLink: return 256;          // N = 256
     case ED_CELL_TAGGER: return 256;            // N = 256
     case kCellMvP: return 256;                  // N = 256
@@ -150,6 +154,8 @@ inline bool cell_implemented(int cell) {
     case ED_CELL_TAGGER:
     case ED_CELL_LATTICE_CHAR:
     case ED_CELL_LATTICE_WORD:
+    case ED_CELL_LATTICEGRU_CHAR:
+    case ED_CELL_LATTICEGRU_WORD:
     case ED_CELL_MVRNN_INTERNAL: return true;
     default: return false;
   }

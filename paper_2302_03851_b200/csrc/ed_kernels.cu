@@ -263,8 +263,12 @@ __device__ __forceinline__ void stamp_step(const KParams &p, int s) {
 
 // optional phase trace of CTA 0 (profiling aid)
 // phase stamps of the CTA that runs item 0 of each step (profiling aid; off unless io.trace is set)
+#ifdef ED_NO_TRACE
+#define ED_TRACE(p, s, k, first) do { } while (0)
+#else
 #define ED_TRACE(p, s, k, first) \
   do { if ((p).trace && (first)) (p).trace[(s) * 64 + (k)] = globaltimer(); } while (0)
+#endif
 
 // ------------------------------------------------------------------------------------------------
 // cell math — one hidden unit, fp32
@@ -329,7 +333,8 @@ __device__ __forceinline__ const T *segment_row(const KParams &p, const DevStep 
   const DevWeightSet &w = p.w[st.wset];
   const int cell = st.cell;
   const bool ext_first = (cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF ||
-                          cell == ED_CELL_LSTM || cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD);
+                          cell == ED_CELL_LSTM || cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD ||
+                          cell == ED_CELL_LATTICEGRU_CHAR || cell == ED_CELL_LATTICEGRU_WORD);
   if (ext_first) {
     if (s == 0) {
       const int tok = __ldg(p.idx + st.ext_off + i);
@@ -345,7 +350,8 @@ __device__ __forceinline__ const T *segment_row(const KParams &p, const DevStep 
 
 __device__ __forceinline__ bool ext_first_cell(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREEGRU_LEAF || cell == ED_CELL_LSTM ||
-         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD;
+         cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == ED_CELL_LATTICEGRU_CHAR ||
+         cell == ED_CELL_LATTICEGRU_WORD;
 }
 // Operand entry of K segment s for member i: >= 0 row of H; < 0 embedding row (-1 - id).
 __device__ __forceinline__ int segment_entry(const KParams &p, const DevStep &st, int s, int i) {
@@ -428,6 +434,22 @@ __device__ __forceinline__ void cell_epilogue(const KParams &p, const DevStep &s
       const int eb = slot_entry(st, p.idx, 0, i);
       c = act_sig<T>(z[1]) * c_of(p, eb, j) + act_sig<T>(z[0]) * act_tanh<T>(z[2]);
       hv = c;
+      break;
+    }
+    case ED_CELL_LATTICEGRU_CHAR:
+    case ED_CELL_LATTICEGRU_WORD: {  // GRU [r; z; n_x; n_h] (A-27), char: max-pool with word states
+      const DevWeightSet &w = p.w[st.wset];
+      const int ep = slot_entry(st, p.idx, 0, i);
+      const float hp = to_f<T>(entry_row<T>(p, w, ep, false)[j]);
+      const float rr = act_sig<T>(z[0]), zz = act_sig<T>(z[1]);
+      const float n = act_tanh<T>(z[2] + rr * z[3]);
+      hv = (1.f - zz) * n + zz * hp;
+      if (st.cell == ED_CELL_LATTICEGRU_CHAR) {
+        const int beg = __ldg(p.idx + st.var_off + i), end = __ldg(p.idx + st.var_off + i + 1);
+        for (int k = beg; k < end; ++k)
+          hv = fmaxf(hv, to_f<T>(__ldcg(static_cast<const T *>(p.H) + static_cast<size_t>(__ldg(p.idx + k)) * h + j)));
+      }
+      has_c = false;
       break;
     }
     case kCellLatticeLink:  // l = s(W_l [x_e; c^w] + b_l) -> X
@@ -782,6 +804,7 @@ __device__ __forceinline__ bool is_umma_cell(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
          cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == kCellLatticeLink ||
+         cell == ED_CELL_LATTICEGRU_CHAR || cell == ED_CELL_LATTICEGRU_WORD ||
          cell == ED_CELL_TAGGER || cell == kCellMvP || cell == kCellMvMat;
 }
 
@@ -799,6 +822,8 @@ template <> struct CellCfg<ED_CELL_TREEFC_INTERNAL> { static constexpr int G = 1
 template <> struct CellCfg<ED_CELL_LSTM> { static constexpr int G = 4, U = 64, NC = 1, NH = 0; };
 template <> struct CellCfg<ED_CELL_LATTICE_CHAR> { static constexpr int G = 4, U = 64, NC = 1, NH = 0; };
 template <> struct CellCfg<ED_CELL_LATTICE_WORD> { static constexpr int G = 3, U = 80, NC = 1, NH = 0; };
+template <> struct CellCfg<ED_CELL_LATTICEGRU_CHAR> { static constexpr int G = 4, U = 64, NC = 0, NH = 1; };
+template <> struct CellCfg<ED_CELL_LATTICEGRU_WORD> { static constexpr int G = 4, U = 64, NC = 0, NH = 1; };
 template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 template <> struct CellCfg<kCellMvP> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
@@ -868,7 +893,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   const uint4 *hp1 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e1) * h + jb);
   // lattice char: words ending here (variadic inputs)
   int wbeg = 0, wend = 0;
-  if constexpr (CELL == ED_CELL_LATTICE_CHAR) {
+  if constexpr (CELL == ED_CELL_LATTICE_CHAR || CELL == ED_CELL_LATTICEGRU_CHAR) {
     if (valid) {
       wbeg = __ldg(p.idx + st.var_off + i);
       wend = __ldg(p.idx + st.var_off + i + 1);
@@ -916,7 +941,8 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       z[g][4] += b1.x; z[g][5] += b1.y; z[g][6] += b1.z; z[g][7] += b1.w;
     }
     constexpr bool HAS_C = !(CELL == ED_CELL_TREEGRU_LEAF || CELL == ED_CELL_TREEGRU_INTERNAL ||
-                             CELL == ED_CELL_TREEFC_INTERNAL || CELL == ED_CELL_TAGGER || CELL == kCellMvP);
+                             CELL == ED_CELL_TREEFC_INTERNAL || CELL == ED_CELL_TAGGER || CELL == kCellMvP ||
+                             CELL == ED_CELL_LATTICEGRU_CHAR || CELL == ED_CELL_LATTICEGRU_WORD);
     constexpr bool HAS_H = CELL != kCellLatticeLink;
     float hv[8] = {}, cv[8] = {};
     float hl[8], hr[8];
@@ -984,9 +1010,23 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
           hv[k] = cv[k];
         } else if constexpr (CELL == kCellLatticeLink) {  // l = s(.) -> X
           cv[k] = sigm_fast(z[0][k]);
+        } else if constexpr (CELL == ED_CELL_LATTICEGRU_CHAR || CELL == ED_CELL_LATTICEGRU_WORD) {
+          // GRU (A-27): [r; z; n_x; n_h]; n = tanh(n_x + r * n_h); h = (1 - z) n + z h_prev
+          const float rr = sigm_fast(z[0][k]), zz = sigm_fast(z[1 % G][k]);
+          const float n = tanh_fast(z[2 % G][k] + rr * z[3 % G][k]);
+          hv[k] = (1.f - zz) * n + zz * hl[k];
         } else {  // tagger hidden t = tanh(.), MV-RNN p = tanh(.) -> H
           hv[k] = tanh_fast(z[0][k]);
         }
+      }
+    }
+    if constexpr (CELL == ED_CELL_LATTICEGRU_CHAR) {  // max-pool with the states of words ending here
+      for (int w = wbeg; w < wend; ++w) {
+        const int wr = __ldg(p.idx + w);
+        float hw[8];
+        unpack_bf16x8(__ldcg(reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(wr) * h + j0)), hw);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hv[k] = fmaxf(hv[k], hw[k]);
       }
     }
     if constexpr (HAS_H) {
@@ -1171,7 +1211,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
       const bool bias_smem = bsrc != nullptr && st.gates * h * 4 <= kBiasBytes;
+#ifdef ED_SCALAR_BIAS
+      if (bias_smem)
+        for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
+      if (false) {
+#else
       if (bias_smem) {  // float4 loads issued back to back (G*h/4 <= 640 -> <= 5 per thread)
+#endif
         const int n4 = st.gates * h / 4;
         const float4 *b4 = reinterpret_cast<const float4 *>(bsrc);
         float4 tmp[5];
@@ -1204,6 +1250,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_CHAR:
             umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+          case ED_CELL_LATTICEGRU_CHAR:
+            umma_epilogue<ED_CELL_LATTICEGRU_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+          case ED_CELL_LATTICEGRU_WORD:
+            umma_epilogue<ED_CELL_LATTICEGRU_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_WORD:
             umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellLatticeLink:
@@ -1366,9 +1416,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
         int cb[2] = {-1, -1};  // per K segment: base row of its contiguous block, or -1 (gathered)
+#ifndef ED_NO_HOIST
 #pragma unroll
         for (int sg = 0; sg < 2; ++sg)
           if (sg < nseg && !segment_contig(p, st, sg, &cb[sg])) cb[sg] = -1;
+#endif
         for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
           const int nk = min(kps, kc_total - kc0);
           const uint32_t stg = pipe.it % kStages;
@@ -1389,7 +1441,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           const int kc = kc0;
           const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
           uint8_t *a_dst = stages + stg * kStageBytes;
+#ifdef ED_NO_HOIST
+          int cbase = -1;
+          if (!segment_contig(p, st, seg, &cbase)) cbase = -1;
+#else
           const int cbase = seg == 0 ? cb[0] : cb[1];
+#endif
           if (cbase >= 0) {
             if (lt == 0) {
               mbar_arrive_tx(full + stg, kAStage);
@@ -1470,6 +1527,7 @@ static bool umma_cell_host(int cell) {
   return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
          cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == ED_CELL_TAGGER ||
+         cell == ED_CELL_LATTICEGRU_CHAR || cell == ED_CELL_LATTICEGRU_WORD ||
          cell == ED_CELL_MVRNN_INTERNAL;
 }
 

@@ -27,7 +27,7 @@ STATUS = {0: "ED_OK", -1: "ED_E_INVALID_ARG", -2: "ED_E_CYCLE", -3: "ED_E_DANGLI
           -10: "ED_E_WORKSPACE", -11: "ED_E_OOM"}
 CELL = {"treelstm_leaf": 1, "treelstm_internal": 2, "linear_out": 3, "treegru_leaf": 4,
         "treegru_internal": 5, "treefc_internal": 6, "lstm": 7, "tagger": 8, "mvrnn_internal": 9,
-        "lattice_char": 10, "lattice_word": 11}
+        "lattice_char": 10, "lattice_word": 11, "latticegru_char": 12, "latticegru_word": 13}
 DTYPE = {"fp32": ED_FP32, "bf16": ED_BF16}
 
 _p = ctypes.POINTER

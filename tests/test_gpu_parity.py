@@ -196,3 +196,14 @@ def test_treelstm_2type_with_learned_fsm():
     assert all(v <= TOL[wl.dtype] for v in err.values()), err
     prio = E.ed_plan(wl.graphs, wl.types, E.fsm_from_priority(wl.priority, len(wl.types)))
     assert plan.info["num_batches"] <= prio.info["num_batches"]
+
+
+@pytest.mark.parametrize("dtype,h", [("bf16", 128), ("fp32", 64)])
+def test_latticegru(dtype, h):
+    """LatticeGRU (A-27): GRU char cells max-pooled with word GRU states."""
+    _check(W.lattice(40, (1, 40), h, dtype, cfg=49, cell="latticegru"))
+
+
+def test_cfg5_latticegru_full_size_sampled():
+    wl = W.config("cfg5_gru")
+    _check(wl, list(range(0, 512, 37)))

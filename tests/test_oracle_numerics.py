@@ -239,6 +239,7 @@ def test_linear_out_selects_units():
     lambda: W.treefc(5, (1, 9), 6, "fp32", cfg=4, cell="mvrnn"),
     lambda: W.bilstm(4, (3, 9), 8, "fp32", cfg=2),
     lambda: W.lattice(5, (3, 14), 8, "fp32", cfg=5),
+    lambda: W.lattice(6, (3, 14), 8, "fp32", cfg=6, cell="latticegru"),
 ])
 def test_two_evaluators_agree(wlf):
     wl = wlf()
@@ -253,3 +254,48 @@ def test_two_evaluators_agree(wlf):
                     np.testing.assert_allclose(ra[key], rb[key], rtol=0, atol=1e-12)
                     n += 1
     assert n > 0
+
+
+
+def _gru_stacked(gen, h):
+    """torch GRUCell weights and the equivalent stacked [r; z; n_x; n_h] over [x; h] (A-27)."""
+    wi, wh = _rand(gen, 3 * h, h), _rand(gen, 3 * h, h)
+    bi, bh = _rand(gen, 3 * h), _rand(gen, 3 * h)
+    W = np.zeros((4 * h, 2 * h))
+    W[:h, :h], W[:h, h:] = wi[:h], wh[:h]                   # r
+    W[h:2 * h, :h], W[h:2 * h, h:] = wi[h:2 * h], wh[h:2 * h]  # z
+    W[2 * h:3 * h, :h] = wi[2 * h:]                          # n_x
+    W[3 * h:, h:] = wh[2 * h:]                               # n_h
+    b = np.concatenate([bi[:h] + bh[:h], bi[h:2 * h] + bh[h:2 * h], bi[2 * h:], bh[2 * h:]])
+    cell = torch.nn.GRUCell(h, h).double()
+    with torch.no_grad():
+        cell.weight_ih.copy_(torch.tensor(wi)); cell.weight_hh.copy_(torch.tensor(wh))
+        cell.bias_ih.copy_(torch.tensor(bi)); cell.bias_hh.copy_(torch.tensor(bh))
+    return {"W": W, "b": b}, cell
+
+
+def test_latticegru_word_and_wordless_char_equal_grucell():
+    """A-27: the LatticeGRU word cell, and a char cell with no word ending at it, are torch GRUCell."""
+    gen = np.random.default_rng(11)
+    h = 6
+    p, cell = _gru_stacked(gen, h)
+    x, hp = _rand(gen, h), _rand(gen, h)
+    with torch.no_grad():
+        ref = cell(torch.tensor(x)[None], torch.tensor(hp)[None])[0].numpy()
+    np.testing.assert_allclose(cells.latticegru_word(p, x, hp), ref, atol=1e-14)
+    np.testing.assert_allclose(cells.latticegru_char(p, x, hp, []), ref, atol=1e-14)
+
+
+def test_latticegru_char_max_pools_word_states():
+    """A-27: with words ending at the char, h = element-wise max of the GRU state and the word states."""
+    gen = np.random.default_rng(12)
+    h = 4
+    p, cell = _gru_stacked(gen, h)
+    x, hp = _rand(gen, h), _rand(gen, h)
+    with torch.no_grad():
+        g = cell(torch.tensor(x)[None], torch.tensor(hp)[None])[0].numpy()
+    w1 = np.array([10.0, -10.0, 10.0, -10.0])
+    w2 = np.array([-10.0, 10.0, -10.0, -10.0])
+    out = cells.latticegru_char(p, x, hp, [w1, w2])
+    np.testing.assert_array_equal(out[:3], [10.0, 10.0, 10.0])
+    np.testing.assert_allclose(out[3], g[3], atol=1e-14)

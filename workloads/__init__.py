@@ -181,7 +181,7 @@ def bichain_graph(length: int, tok: SplitMix64, vocab: int, t_f: int, t_b: int, 
 
 
 def lattice_graph(n_chars: int, rng: SplitMix64, tok: SplitMix64, char_vocab: int, word_vocab: int,
-                  t_char: int, t_word: int, p_word: float = 0.3) -> Graph:
+                  t_char: int, t_word: int, p_word: float = 0.3, word_end_char: bool = True) -> Graph:
     """Lattice(n) (PAPER Fig. 7): char chain plus word skip cells.
 
     Word W(b->e), e = min(n-1, b+L-1), L ~ U{2,3,4}, added with probability p for b in 0..n-2;
@@ -209,7 +209,8 @@ def lattice_graph(n_chars: int, rng: SplitMix64, tok: SplitMix64, char_vocab: in
         char_id.append(bld.add(t_char, slots, chars[e]))
         for w in words:
             if w[0] == e:
-                word_id[w] = bld.add(t_word, [char_id[e], -1 - chars[w[1]]], word_tok[w])
+                slots = [char_id[e], -1 - chars[w[1]]] if word_end_char else [char_id[e]]
+                word_id[w] = bld.add(t_word, slots, word_tok[w])
                 ends.setdefault(w[1], []).append(w)
     return bld.build(char_id[-1])
 
@@ -272,6 +273,13 @@ def make_params(kind: str, h: int, gen: np.random.Generator, vocab: int = 0, out
         p["mat"] = (eye[None, :, :] + _uniform(gen, (vocab, h, h), 0.01)).astype(np.float32)
     elif kind == "lattice_char":
         p["W"] = _uniform(gen, (4 * h, 2 * h), s); p["b"] = _uniform(gen, (4 * h,), s)
+        p["emb"] = _uniform(gen, (vocab, h), 1.0)
+    elif kind in ("latticegru_char", "latticegru_word"):
+        # GRUCell weights stacked over [x; h]: rows [r; z; n_x; n_h]; n_x reads x only, n_h h only
+        W = _uniform(gen, (4 * h, 2 * h), s)
+        W[2 * h:3 * h, h:] = 0.0
+        W[3 * h:, :h] = 0.0
+        p["W"] = W; p["b"] = _uniform(gen, (4 * h,), s)
         p["emb"] = _uniform(gen, (vocab, h), 1.0)
     elif kind == "lattice_word":
         p["W"] = _uniform(gen, (3 * h, 2 * h), s); p["b"] = _uniform(gen, (3 * h,), s)
@@ -384,10 +392,22 @@ def bilstm(n_seqs: int, lengths: tuple, h: int, dtype: str, cfg: int = 2, vocab:
 
 
 def lattice(n_lattices: int, chars: tuple, h: int, dtype: str, cfg: int = 5, char_vocab: int = 4096,
-            word_vocab: int = 16384, p_word: float = 0.3, priority=(0, 1)) -> Workload:
-    """LatticeLSTM: types C (char cell, variadic word inputs) and W (word cell)."""
+            word_vocab: int = 16384, p_word: float = 0.3, priority=(0, 1), cell: str = "lattice") -> Workload:
+    """LatticeLSTM (cell="lattice") or LatticeGRU (cell="latticegru", A-27): types C (char cell,
+    variadic word inputs) and W (word cell); same topology (Fig. 7)."""
     rng = SplitMix64(1000 + cfg)
     tok = SplitMix64(3000 + cfg)
+    if cell == "latticegru":
+        types = [OpType("C", "latticegru_char", 1, variadic=1, has_ext=1, weight_set=0, hidden=h, dtype=dtype),
+                 OpType("W", "latticegru_word", 1, has_ext=1, weight_set=1, hidden=h, dtype=dtype)]
+        graphs = [lattice_graph(rng.randint(chars[0], chars[1]), rng, tok, char_vocab, word_vocab, 0, 1, p_word,
+                                word_end_char=False) for _ in range(n_lattices)]
+        gen = np.random.default_rng(2000 + cfg)
+        params = [make_params("latticegru_char", h, gen, vocab=char_vocab),
+                  make_params("latticegru_word", h, gen, vocab=word_vocab)]
+        return Workload(name=f"latticegru_h{h}_{dtype}", types=types, graphs=graphs, priority=list(priority),
+                        params=_finish_params(params, dtype), dtype=dtype, hidden=h,
+                        config={"instances": n_lattices, "chars": list(chars), "cfg": cfg})
     types = [OpType("C", "lattice_char", 1, variadic=1, has_ext=1, weight_set=0, hidden=h, dtype=dtype),
              OpType("W", "lattice_word", 2, has_ext=1, weight_set=1, hidden=h, dtype=dtype)]
     graphs = [lattice_graph(rng.randint(chars[0], chars[1]), rng, tok, char_vocab, word_vocab, 0, 1, p_word)
@@ -420,6 +440,8 @@ def config(name: str) -> Workload:
         return treefc(1024, (5, 40), 512, "bf16", 4, cell="mvrnn")
     if name == "cfg5":
         return lattice(512, (10, 50), 256, "bf16", 5)
+    if name == "cfg5_gru":
+        return lattice(512, (10, 50), 256, "bf16", 5, cell="latticegru")
     if name == "cfg5_h512":
         return lattice(512, (10, 50), 512, "bf16", 5)
     raise KeyError(name)
