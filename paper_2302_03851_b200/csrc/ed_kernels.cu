@@ -1181,18 +1181,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
       const int C = st.gates;
       const bool in_smem = C * h * 4 <= kWoutBytes;
-      if (in_smem) {  // float4 loads issued back to back (C*h/4 <= 768 -> <= 2 per thread)
-        const float4 *W4 = static_cast<const float4 *>(step_W(p, st));
-        const int n4 = C * h / 4;
-        float4 tmp[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (tid + u * kThreadsTC < n4) tmp[u] = __ldg(W4 + tid + u * kThreadsTC);
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (tid + u * kThreadsTC < n4) reinterpret_cast<float4 *>(swout)[tid + u * kThreadsTC] = tmp[u];
+      if (in_smem) {  // 16 B cp.async per piece (no register staging)
+        const float *W = static_cast<const float *>(step_W(p, st));
+        const uint32_t sw = smem_u32(swout);
+        for (int q = tid; q < C * h / 4; q += kThreadsTC) cp_async16(sw + 16u * q, W + 4 * q);
+        cp_async_commit();
+        cp_async_wait<0>();
       }
-      if (p.trace && tid == 0) p.trace[p.num_steps * 64 + blockIdx.x * 4 + 0] = globaltimer();
       __syncthreads();
       if (p.trace && tid == 0) p.trace[p.num_steps * 64 + blockIdx.x * 4 + 1] = globaltimer();
       const float *Ws = in_smem ? swout : static_cast<const float *>(step_W(p, st));
@@ -1211,22 +1206,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
       const bool bias_smem = bsrc != nullptr && st.gates * h * 4 <= kBiasBytes;
-#ifdef ED_SCALAR_BIAS
-      if (bias_smem)
-        for (int q = tid; q < st.gates * h; q += kEpiThreads) sbias[q] = bsrc[q];
-      if (false) {
-#else
-      if (bias_smem) {  // float4 loads issued back to back (G*h/4 <= 640 -> <= 5 per thread)
-#endif
-        const int n4 = st.gates * h / 4;
-        const float4 *b4 = reinterpret_cast<const float4 *>(bsrc);
-        float4 tmp[5];
-#pragma unroll
-        for (int u = 0; u < 5; ++u)
-          if (tid + u * kEpiThreads < n4) tmp[u] = __ldg(b4 + tid + u * kEpiThreads);
-#pragma unroll
-        for (int u = 0; u < 5; ++u)
-          if (tid + u * kEpiThreads < n4) reinterpret_cast<float4 *>(sbias)[tid + u * kEpiThreads] = tmp[u];
+      if (bias_smem) {  // 16 B cp.async per piece: no register staging, all pieces in flight at once
+        const uint32_t sb = smem_u32(sbias);
+        for (int q = tid; q < st.gates * h / 4; q += kEpiThreads) cp_async16(sb + 16u * q, bsrc + 4 * q);
+        cp_async_commit();
+        cp_async_wait<0>();
       }
       asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
       const float *bias = bias_smem ? sbias : bsrc;
