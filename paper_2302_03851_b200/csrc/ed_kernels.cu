@@ -212,11 +212,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // step_contrib over the device steps that write it (h per row-vector result, h*h for a matrix).  A consumer acquires ready[row] >= target[row] before reading
 // the row; a producer publishes with a release-add after its stores.  Rows are only produced by
 // earlier device steps and every warp walks the steps in order, so waiting cannot deadlock.
-__device__ __forceinline__ int ld_relaxed_s32(const int *a) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
 __device__ __forceinline__ int ld_acquire_s32(const int *a) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
@@ -230,11 +225,7 @@ __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep 
   if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
   if (need <= 0) return;
   unsigned spins = 0;
-#ifdef ED_RELAXED_POLL
-  while (ld_relaxed_s32(p.ready + e) < need) {
-#else
   while (ld_acquire_s32(p.ready + e) < need) {
-#endif
     if (++spins > (1u << 26)) {  // watchdog: report the stuck dependency, then abort the launch
       printf("ed_batch watchdog: block %d thread %d cell %d out_row0 %d row %d ready %d need %d\n", blockIdx.x,
              threadIdx.x, st.cell, st.out_row0, e, ld_acquire_s32(p.ready + e), need);
@@ -248,11 +239,7 @@ __device__ __forceinline__ bool row_ready(const KParams &p, int e, const DevStep
   if (e < 0 || e >= p.rows) return true;
   int need = __ldg(p.target + e);
   if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
-#ifdef ED_RELAXED_POLL
-  return need <= 0 || ld_relaxed_s32(p.ready + e) >= need;
-#else
   return need <= 0 || ld_acquire_s32(p.ready + e) >= need;
-#endif
 }
 __device__ __forceinline__ void publish_row(const KParams &p, int row, int units) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + row), "r"(units) : "memory");
@@ -1400,11 +1387,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
         int cb[2] = {-1, -1};  // per K segment: base row of its contiguous block, or -1 (gathered)
-#ifndef ED_NO_HOIST
 #pragma unroll
         for (int sg = 0; sg < 2; ++sg)
           if (sg < nseg && !segment_contig(p, st, sg, &cb[sg])) cb[sg] = -1;
-#endif
         for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
           const int nk = min(kps, kc_total - kc0);
           const uint32_t stg = pipe.it % kStages;
@@ -1425,12 +1410,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           const int kc = kc0;
           const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
           uint8_t *a_dst = stages + stg * kStageBytes;
-#ifdef ED_NO_HOIST
-          int cbase = -1;
-          if (!segment_contig(p, st, seg, &cbase)) cbase = -1;
-#else
           const int cbase = seg == 0 ? cb[0] : cb[1];
-#endif
           if (cbase >= 0) {
             if (lt == 0) {
               mbar_arrive_tx(full + stg, kAStage);
