@@ -30,8 +30,11 @@ namespace ed {
 // constants of the bf16 tensor-core engine
 // ------------------------------------------------------------------------------------------------
 constexpr int kThreads = 256;        // fp32 SIMT kernel
-constexpr int kThreadsTC = 384;      // bf16 tensor-core kernel: 4 epilogue, MMA, B, 6 A-loader warps
-constexpr int kLoaderThreads = 192;  // warps 6..11
+#ifndef ED_LOADER_WARPS
+#define ED_LOADER_WARPS 6
+#endif
+constexpr int kLoaderThreads = ED_LOADER_WARPS * 32;  // warps 6.. (operand gathers)
+constexpr int kThreadsTC = 192 + kLoaderThreads;      // bf16 tensor-core kernel: 4 epilogue, MMA, B, loaders
 constexpr int kStages = 4;
 constexpr int kTileM = 128;
 constexpr int kChunkK = 64;                  // bf16 elements per 128 B swizzle row
