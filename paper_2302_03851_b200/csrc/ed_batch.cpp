@@ -127,6 +127,7 @@ struct ed_plan_s {
   int64_t V = 0;
   int32_t ninst = 0;
   std::vector<int32_t> gtype, in_off, in_idx, ext;  // in_idx: >=0 global node, ZERO, or -1-id external
+  std::vector<int32_t> indeg, coff, cons;  // node-input counts and consumers CSR (from validation)
   std::vector<int32_t> roots;                         // global node id or -1-id
   // schedule
   std::vector<int32_t> batch_type, batch_off, members;
@@ -218,14 +219,17 @@ static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, i
     pl->roots[gi] = g.root >= 0 ? static_cast<int32_t>(base + g.root) : g.root;
     base += n;
   }
-  // acyclicity (Kahn)
-  std::vector<int32_t> indeg(total, 0);
-  std::vector<int32_t> coff(total + 1, 0);
+  // acyclicity (Kahn); the consumers CSR and in-degrees are kept for Alg. 1
+  std::vector<int32_t> &indeg = pl->indeg;
+  std::vector<int32_t> &coff = pl->coff;
+  indeg.assign(total, 0);
+  coff.assign(total + 1, 0);
   for (int64_t v = 0; v < total; ++v)
     for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
       if (pl->in_idx[k] >= 0) { ++indeg[v]; ++coff[pl->in_idx[k] + 1]; }
   for (int64_t v = 0; v < total; ++v) coff[v + 1] += coff[v];
-  std::vector<int32_t> cons(coff[total]);
+  std::vector<int32_t> &cons = pl->cons;
+  cons.assign(coff[total], 0);
   {
     std::vector<int32_t> fill(coff.begin(), coff.end() - 1);
     for (int64_t v = 0; v < total; ++v)
@@ -276,19 +280,9 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
       table[key] = en.action;
     }
   }
-  // consumers CSR and remaining-input counters (one count per node-input edge)
-  std::vector<int32_t> remaining(V, 0), coff(V + 1, 0);
-  for (int64_t v = 0; v < V; ++v)
-    for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
-      if (pl->in_idx[k] >= 0) { ++remaining[v]; ++coff[pl->in_idx[k] + 1]; }
-  for (int64_t v = 0; v < V; ++v) coff[v + 1] += coff[v];
-  std::vector<int32_t> cons(coff[V]);
-  {
-    std::vector<int32_t> fill(coff.begin(), coff.end() - 1);
-    for (int64_t v = 0; v < V; ++v)
-      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
-        if (pl->in_idx[k] >= 0) cons[fill[pl->in_idx[k]]++] = static_cast<int32_t>(v);
-  }
+  // consumers CSR and remaining-input counters (one count per node-input edge), from validation
+  std::vector<int32_t> remaining(pl->indeg);
+  const std::vector<int32_t> &coff = pl->coff, &cons = pl->cons;
   std::vector<std::vector<int32_t>> ready(nt);
   for (int64_t v = 0; v < V; ++v)
     if (remaining[v] == 0) ready[pl->gtype[v]].push_back(static_cast<int32_t>(v));
@@ -325,20 +319,23 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
     pl->batch_off.push_back(static_cast<int32_t>(pl->members.size()));
   }
   // App. B.3 lower bound: per type, the max number of type-t nodes on a path (= Depth(G^t)).
-  std::vector<int32_t> topo(pl->members);  // schedule order is a topological order
+  // one pass over the schedule order (a topological order) with nt counters per node
   int64_t lb = 0;
-  std::vector<int32_t> cnt(V);
-  for (int t = 0; t < nt; ++t) {
-    int32_t best = 0;
-    for (int32_t v : topo) {
-      int32_t c = 0;
-      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
-        if (pl->in_idx[k] >= 0) c = std::max(c, cnt[pl->in_idx[k]]);
-      cnt[v] = c + (pl->gtype[v] == t ? 1 : 0);
-      best = std::max(best, cnt[v]);
+  std::vector<int32_t> cnt(static_cast<size_t>(V) * nt, 0), best(nt, 0), c(nt);
+  for (int32_t v : pl->members) {
+    std::fill(c.begin(), c.end(), 0);
+    for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+      if (pl->in_idx[k] >= 0) {
+        const int32_t *cu = &cnt[static_cast<size_t>(pl->in_idx[k]) * nt];
+        for (int t = 0; t < nt; ++t) c[t] = std::max(c[t], cu[t]);
+      }
+    int32_t *cv = &cnt[static_cast<size_t>(v) * nt];
+    for (int t = 0; t < nt; ++t) {
+      cv[t] = c[t] + (pl->gtype[v] == t ? 1 : 0);
+      best[t] = std::max(best[t], cv[t]);
     }
-    lb += best;
   }
+  for (int t = 0; t < nt; ++t) lb += best[t];
   pl->lower_bound = lb;
   return ED_OK;
 }
