@@ -204,6 +204,37 @@ class ClockSampler:
 
 
 # --- CPU oracle baseline (bounded sample) -------------------------------------------------------
+def latency_floor_us(E, wl, depth: int = 24):
+    """SURVEY §8(d) latency floor: the per-step cost of the same persistent kernel on a chain of
+    dependent one-row batches (a caterpillar tree of the workload's cell types: each internal node
+    reads the previous one and a fresh leaf), i.e. readiness propagation + operand load + K chain +
+    epilogue with no parallel work.  Median in-kernel step time of the internal steps.  Only for the
+    tree workloads (L, I[, I2], O types)."""
+    import numpy as np
+    import torch
+    names = [t.name for t in wl.types]
+    if names[:2] != ["L", "I"] and names[:2] != ["L", "I1"]:
+        return None
+    types, ins, ext = [], [], []
+    types.append(0); ins.append([]); ext.append(1)
+    prev = 0
+    for k in range(depth):
+        types.append(0); ins.append([]); ext.append(2 + k)
+        leaf = len(types) - 1
+        types.append(1); ins.append([prev, leaf]); ext.append(-1)
+        prev = len(types) - 1
+    g = W.graph_from_lists(types, ins, ext, root=prev)
+    plan = E.ed_plan([g], wl.types[:2], E.fsm_from_priority([0, 1], 2))
+    weights = E.DeviceWeights(wl.types[:2], wl.params[:2])
+    ws = E.Workspace(plan)
+    out = torch.zeros(1, wl.hidden, dtype=torch.bfloat16 if wl.dtype == "bf16" else torch.float32, device="cuda")
+    for _ in range(4):
+        E.ed_execute(plan, weights, ws, out)
+    torch.cuda.synchronize()
+    st = ws.step_times_ns()
+    return float(np.median(st[1:])) / 1e3 if len(st) > 2 else None
+
+
 def cpu_oracle_rate(wl, seconds: float, max_instances: int = 256):
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle.evaluate import evaluate_recursive
@@ -381,8 +412,14 @@ def main():
         if os.path.exists(prof):
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         meas = [x / 1e9 for x in step_ns]
+        t_floor = latency_floor_us(E, wl) if world == 1 or rank == 0 else None
         per_step = {"sum_t_roof_us": 1e6 * sum(troof), "sum_t_meas_us": 1e6 * sum(meas),
                     "frac": (sum(troof) / sum(meas)) if sum(meas) > 0 else None,
+                    # secondary: per-step latency floor of the persistent kernel and the
+                    # "achievable" fraction sum max(t_roof, t_floor) / sum t_meas
+                    "t_floor_us": t_floor,
+                    "achievable_frac": (sum(max(1e6 * r, t_floor) for r in troof) / (1e6 * sum(meas)))
+                    if (t_floor and sum(meas) > 0) else None,
                     "steps": [{"type": wl.types[t].name, "m": len(mem), "t_roof_us": round(1e6 * r, 3),
                                "t_meas_us": round(1e6 * s_, 3)}
                               for (t, mem), r, s_ in zip(plan.schedule(), troof, meas)]}
