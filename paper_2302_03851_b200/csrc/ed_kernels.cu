@@ -1096,7 +1096,7 @@ __device__ __forceinline__ int step_items(const DevStep &st, int h) {
 }
 // K chunks per pipeline stage.  One full/empty mbarrier round costs ~0.3 us whatever its payload
 // (scripts/loop_probe.cu), so a small tile (m <= 120 rows: A chunk = round8(m) x 128 B) packs
-// several K chunks into one 48 KB stage: chunk q's A at q * abytes, its B at 16 KB + q * N * 128 B.
+// several K chunks into one 48 KB stage: chunk q's A at q * abytes, its B at kps * abytes + q * N * 128 B.
 // M = 128 MMAs read 128 A rows from q * abytes; rows past the tile's m are never stored.
 #ifndef ED_KPS_MAX
 #define ED_KPS_MAX 16
@@ -1106,7 +1106,8 @@ __device__ __forceinline__ int step_kps(const DevStep &st, int kc_total, uint32_
   const int rows = min(kTileM, (st.m + 7) & ~7);
   *abytes = static_cast<uint32_t>(rows) * 128u;
   const int bb = st.gates * st.units * 128;
-  const int k = min(kAStage / static_cast<int>(*abytes), kBStage / bb);
+  // small tiles: the 48 KB stage is cut as [A_0 .. A_{k-1} | B_0 .. B_{k-1}], k = 48 KB / (A + B chunk)
+  const int k = *abytes < static_cast<uint32_t>(kAStage) ? kStageBytes / (static_cast<int>(*abytes) + bb) : 1;
   return max(1, min(min(k, kc_total), ED_KPS_MAX));
 }
 __device__ __forceinline__ int first_item(uint32_t off) {
@@ -1191,6 +1192,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
     uint32_t abytes = kAStage;
     const int kps = step_kps(st, kc_total, &abytes);
+    const uint32_t boff = kps > 1 ? kps * abytes : static_cast<uint32_t>(kAStage);  // B region of a stage
     const uint32_t bchunk = static_cast<uint32_t>(ncols) * 128u;
     if (warp < 4) {
       // ---------------- epilogue warps ----------------
@@ -1264,7 +1266,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             ED_TRACE(p, s, 3, kc0 == 0 && t == 0);
             const uint32_t sbase = smem_u32(stages + stg * kStageBytes);
             for (int q = 0; q < nk; ++q) {
-              const uint64_t ad = sw128_desc(sbase + q * abytes), bd = sw128_desc(sbase + kAStage + q * bchunk);
+              const uint64_t ad = sw128_desc(sbase + q * abytes), bd = sw128_desc(sbase + boff + q * bchunk);
 #pragma unroll
               for (int k = 0; k < kChunkK / 16; ++k)
                 tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc0 + q > 0 || k > 0) ? 1u : 0u);
@@ -1294,7 +1296,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             for (int q = 0; q < nk; ++q) {
               const uint8_t *src =
                   Wp + ((static_cast<size_t>(kc0 + q) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-              bulk_g2s(stages + stg * kStageBytes + kAStage + q * bchunk, src, nb, full + stg);
+              bulk_g2s(stages + stg * kStageBytes + boff + q * bchunk, src, nb, full + stg);
             }
             ++pipe.it;
           }
