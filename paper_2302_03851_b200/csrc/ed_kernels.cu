@@ -1415,7 +1415,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           const int kc = kc0;
           const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
           uint8_t *a_dst = stages + stg * kStageBytes;
-          const int cbase = seg == 0 ? cb[0] : cb[1];
+          // a 128-row box needs the full 16 KB A region: only with one chunk per stage (kps == 1)
+          const int cbase = kps == 1 ? (seg == 0 ? cb[0] : cb[1]) : -1;
           if (cbase >= 0) {
             if (lt == 0) {
               mbar_arrive_tx(full + stg, kAStage);

@@ -207,3 +207,11 @@ def test_latticegru(dtype, h):
 def test_cfg5_latticegru_full_size_sampled():
     wl = W.config("cfg5_gru")
     _check(wl, list(range(0, 512, 37)))
+
+
+@pytest.mark.parametrize("h", [192, 128])
+def test_small_contiguous_tiles_with_single_chunk_last_stage(h):
+    """Regression: a small tile (several K chunks per stage) whose last stage holds one chunk of a
+    contiguous operand must gather it, not load a 128-row TMA box over the stage's B region
+    (h = 192: 6 K chunks = stages of 5 + 1 for 8-row tiles)."""
+    _check(W.bilstm(8, (6, 14), h, "bf16", cfg=71, with_tagger=False))
