@@ -104,6 +104,13 @@ __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *m, int
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+// Row-table read as an explicit shared-memory load: a generic LD of a shared address is ordered
+// behind the thread's in-flight cp.async copies, which serialised one L2 round trip per K chunk.
+__device__ __forceinline__ const void *lds_ptr(const void *const *p) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)));
+  return reinterpret_cast<const void *>(v);
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // The mbarrier receives one arrival once every cp.async this thread issued so far has landed (the
 // barrier's expected count includes it: .noinc).
@@ -1407,7 +1414,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
               const uint32_t a_base = smem_u32(stages + stg * kStageBytes) + q * abytes;
               for (int c = lt; c < nrows * 8; c += kLoaderThreads) {
                 const int r = c >> 3, ch = c & 7;
-                const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
+                const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(lds_ptr(tab + r * 2 + seg)) + col0 + ch * 8;
                 cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
               }
             }
@@ -1430,7 +1437,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             const uint32_t a_base = smem_u32(a_dst);
             for (int c = lt; c < nrows * 8; c += kLoaderThreads) {  // rows past m are not loaded
               const int r = c >> 3, ch = c & 7;
-              const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(tab[r * 2 + seg]) + col0 + ch * 8;
+              const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(lds_ptr(tab + r * 2 + seg)) + col0 + ch * 8;
               cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
             }
           }
