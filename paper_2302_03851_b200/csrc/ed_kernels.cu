@@ -111,6 +111,9 @@ __device__ __forceinline__ const void *lds_ptr(const void *const *p) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)));
   return reinterpret_cast<const void *>(v);
 }
+__device__ __forceinline__ void sts_ptr(const void **p, const void *v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(reinterpret_cast<unsigned long long>(v)) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // The mbarrier receives one arrival once every cp.async this thread issued so far has landed (the
 // barrier's expected count includes it: .noinc).
@@ -833,7 +836,7 @@ __device__ __forceinline__ void build_row_table(const KParams &p, const DevStep 
     const int iv = i < st.m ? i : (st.m - 1);
 #pragma unroll
     for (int sg = 0; sg < 2; ++sg)
-      tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H;
+      sts_ptr(tab + r * 2 + sg, sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H);
   }
 }
 
@@ -1376,7 +1379,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           const int iv = i < st.m ? i : (st.m - 1);  // rows past m repeat the last valid row
 #pragma unroll
           for (int sg = 0; sg < 2; ++sg) {
-            tab[r * 2 + sg] = sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H;
+            sts_ptr(tab + r * 2 + sg, sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H);
             ent[nent][sg] = sg < nseg ? segment_entry(p, st, sg, iv) : -1;
           }
         }
