@@ -1401,6 +1401,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA below
         if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
+        const int pieces = nrows * 8;  // 16 B pieces per K chunk
+        const float inv_pieces = 1.0f / static_cast<float>(pieces);
         int cb[2] = {-1, -1};  // per K segment: base row of its contiguous block, or -1 (gathered)
 #pragma unroll
         for (int sg = 0; sg < 2; ++sg)
@@ -1411,19 +1413,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
           if (nk > 1) {  // several small chunks per stage: row gathers only (a 128-row box would overflow)
             if (lt == 0) mbar_arrive(full + stg);
-            for (int q = 0; q < nk; ++q) {
+            // the stage's nk x nrows x 8 pieces spread over all loader threads (a one-row tile puts
+            // its nk chunks on 8 nk lanes at once instead of one chunk after another)
+            const uint32_t a_base = smem_u32(stages + stg * kStageBytes);
+            for (int c = lt; c < nk * pieces; c += kLoaderThreads) {
+              const int q = static_cast<int>((static_cast<float>(c) + 0.5f) * inv_pieces);
+              const int rem = c - q * pieces, r = rem >> 3, ch = rem & 7;
               const int kc = kc0 + q;
-              const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
-              const uint32_t a_base = smem_u32(stages + stg * kStageBytes) + q * abytes;
-              for (int c = lt; c < nrows * 8; c += kLoaderThreads) {
-                const int r = c >> 3, ch = c & 7;
-                const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(lds_ptr(tab + r * 2 + seg)) + col0 + ch * 8;
-                cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
-              }
+              const int seg = kc * kChunkK >= h ? 1 : 0, col0 = kc * kChunkK - seg * h;
+              const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(lds_ptr(tab + r * 2 + seg)) + col0 + ch * 8;
+              cp_async16(a_base + q * abytes + r * 128 + ((ch ^ (r & 7)) << 4), src);
             }
           } else {
           const int kc = kc0;
-          const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
+          const int seg = kc * kChunkK >= h ? 1 : 0, col0 = kc * kChunkK - seg * h;  // K = nseg * h, nseg <= 2
           uint8_t *a_dst = stages + stg * kStageBytes;
           // a 128-row box needs the full 16 KB A region: only with one chunk per stage (kps == 1)
           const int cbase = kps == 1 ? (seg == 0 ? cb[0] : cb[1]) : -1;
