@@ -146,6 +146,22 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged forms: every lane walks the issue loop (operands stay warp-uniform, no per-MMA
+// single-lane R2UR loop) and elect.sync picks the issuing lane.
+__device__ __forceinline__ void tc_mma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
 // 32 lanes x 32 bit, 16 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
   uint32_t r[16];
@@ -1263,33 +1279,32 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       for (int t = t0; t < T; t += G) {
         const uint32_t acc = pipe.ti & 1u;
         const uint32_t idesc = idesc_bf16(st.gates * tile_units(st, h, t % st.n_col_tiles));
-        if (lane == 0) {
-          mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
+        // the whole warp walks the loop (warp-uniform operands); one elected lane issues
+        mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * 256u;
+        const uint64_t astep = abytes >> 4, bstep = bchunk >> 4;  // descriptor address units (16 B)
+        for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
+          const int nk = min(kps, kc_total - kc0);
+          const uint32_t stg = pipe.it % kStages;
+          mbar_wait(full + stg, (pipe.it / kStages) & 1u);
+          fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
           tc_fence_after();
-          const uint32_t d = tmem_base + acc * 256u;
-          for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
-            const int nk = min(kps, kc_total - kc0);
-            const uint32_t stg = pipe.it % kStages;
-            mbar_wait(full + stg, (pipe.it / kStages) & 1u);
-            fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
-            tc_fence_after();
-            ED_TRACE(p, s, 3, kc0 == 0 && t == 0);
-            const uint32_t sbase = smem_u32(stages + stg * kStageBytes);
-            for (int q = 0; q < nk; ++q) {
-              const uint64_t ad = sw128_desc(sbase + q * abytes), bd = sw128_desc(sbase + boff + q * bchunk);
+          ED_TRACE(p, s, 3, lane == 0 && kc0 == 0 && t == 0);
+          const uint32_t sbase = smem_u32(stages + stg * kStageBytes);
+          uint64_t ad = sw128_desc(sbase), bd = sw128_desc(sbase + boff);
+          for (int q = 0; q < nk; ++q, ad += astep, bd += bstep) {
 #pragma unroll
-              for (int k = 0; k < kChunkK / 16; ++k)
-                tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kc0 + q > 0 || k > 0) ? 1u : 0u);
-            }
-            tc_commit(empty + stg);
-            ++pipe.it;
+            for (int k = 0; k < kChunkK / 16; ++k)
+              tc_mma_elect(d, ad + 2 * k, bd + 2 * k, idesc, (kc0 + q > 0 || k > 0) ? 1u : 0u);
           }
-          tc_commit(tfull + acc);
-          ED_TRACE(p, s, 4, t == 0);
+          tc_commit_elect(empty + stg);
+          ++pipe.it;
         }
+        tc_commit_elect(tfull + acc);
+        ED_TRACE(p, s, 4, lane == 0 && t == 0);
         ++pipe.ti;
       }
-      pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
     } else if (warp == 5) {
       // ---------------- weight (B) loader: runs ahead across steps (weights are static) -----------
       const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));

@@ -37,5 +37,4 @@ for s in range(nb):
     rel = lambda k: int(t[s, k] - base) if t[s, k] else None
     print(s, [rel(k) for k in (0, 1, 2, 3, 4, 6, 5)], "|", int(ts[s + 1] - base))
     if len(sys.argv) > 1:
-        print("   Aiss", [rel(k) for k in range(9, 16, 2)], "MMAfull", [rel(k) for k in range(24, 28)],
-              "B", [rel(k) for k in range(32, 36)])
+        print("   mma", [rel(k) for k in range(24, 32)])
