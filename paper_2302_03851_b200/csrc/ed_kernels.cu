@@ -84,10 +84,33 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Warp-converged forms (one elected lane issues; operands warp-uniform)
+__device__ __forceinline__ void mbar_arrive_tx_elect(uint64_t *bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_elect(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // TMA: one box {64 cols, box rows} of a 2-D bf16 tensor at (col, row) -> smem, complete_tx on bar
 __device__ __forceinline__ void tma_row_box(void *dst, const CUtensorMap *m, int col, int row, uint64_t *bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(m), "r"(col), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_row_box_elect(void *dst, const CUtensorMap *m, int col, int row, uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(
           smem_u32(dst)),
       "l"(m), "r"(col), "r"(row), "r"(smem_u32(bar))
       : "memory");
@@ -1309,25 +1332,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- weight (B) loader: runs ahead across steps (weights are static) -----------
       const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
       const size_t ntot = static_cast<size_t>(st.gates) * h;
-      for (int t = t0; t < T; t += G) {
+      for (int t = t0; t < T; t += G) {  // warp-converged; one elected lane issues
         const int col_tile = t % st.n_col_tiles;
-        if (lane == 0) {
-          const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
-          for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
-            const int nk = min(kps, kc_total - kc0);
-            const uint32_t stg = pipe.it % kStages;
-            mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
-            mbar_arrive_tx(full + stg, nb * nk);
-            for (int q = 0; q < nk; ++q) {
-              const uint8_t *src =
-                  Wp + ((static_cast<size_t>(kc0 + q) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-              bulk_g2s(stages + stg * kStageBytes + boff + q * bchunk, src, nb, full + stg);
-            }
-            ++pipe.it;
+        const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
+        for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
+          const int nk = min(kps, kc_total - kc0);
+          const uint32_t stg = pipe.it % kStages;
+          mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+          mbar_arrive_tx_elect(full + stg, nb * nk);
+          for (int q = 0; q < nk; ++q) {
+            const uint8_t *src =
+                Wp + ((static_cast<size_t>(kc0 + q) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
+            bulk_g2s_elect(stages + stg * kStageBytes + boff + q * bchunk, src, nb, full + stg);
           }
+          ++pipe.it;
         }
       }
-      pipe.it = __shfl_sync(0xffffffffu, pipe.it, 0);
     } else {
       // ---------------- operand (A) loaders: warps 6-11 ----------------
       // Per tile: row table (static) -> wait until every input row is published (acquire) ->
@@ -1446,12 +1466,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           // a 128-row box needs the full 16 KB A region: only with one chunk per stage (kps == 1)
           const int cbase = kps == 1 ? (seg == 0 ? cb[0] : cb[1]) : -1;
           if (cbase >= 0) {
-            if (lt == 0) {
-              mbar_arrive_tx(full + stg, kAStage);
+            if (lt < 32) {  // warp-converged; one elected lane issues
+              mbar_arrive_tx_elect(full + stg, kAStage);
               if (st.cell == kCellMvP)  // U rows: [B a | A b], 2h columns
-                tma_row_box(a_dst, &p.tm_u, seg * h + col0, cbase + row_tile * kTileM, full + stg);
+                tma_row_box_elect(a_dst, &p.tm_u, seg * h + col0, cbase + row_tile * kTileM, full + stg);
               else
-                tma_row_box(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
+                tma_row_box_elect(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
             }
           } else {
             if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
