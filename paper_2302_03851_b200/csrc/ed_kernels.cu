@@ -1418,22 +1418,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             ent[nent][sg] = sg < nseg ? segment_entry(p, st, sg, iv) : -1;
           }
         }
-        // readiness of every input row, checked in parallel; block only on the rows still pending
-        // (nothing of this CTA is in flight here: every tile is drained at its end)
-        bool ok = true;
-        for (int q = 0; q < nent; ++q) ok = ok && row_ready(p, ent[q][0], st) && row_ready(p, ent[q][1], st);
-        int all_ok;
-        asm volatile("{\n\t.reg .pred pi, po;\n\tsetp.ne.s32 pi, %1, 0;\n\t"
-                     "bar.red.and.pred po, 1, %2, pi;\n\tselp.s32 %0, 1, 0, po;\n\t}"
-                     : "=r"(all_ok) : "r"(static_cast<int>(ok)), "n"(kLoaderThreads) : "memory");
-        if (!all_ok) {
-          for (int q = 0; q < nent; ++q) {
-            wait_row(p, ent[q][0], st);
-            wait_row(p, ent[q][1], st);
+        // Readiness per K segment, just before its first chunk: the rows of segment sg are checked in
+        // parallel (each thread its own rows, AND-reduced over the loader threads) and the threads
+        // block only on the rows still pending.  A segment that is ready early (an LSTM's x, a leaf
+        // child) is gathered and multiplied while the other segment's producers still run.
+        auto acquire_seg = [&](int sg) {
+          bool ok = true;
+          for (int q = 0; q < nent; ++q) ok = ok && row_ready(p, ent[q][sg], st);
+          int all_ok;
+          asm volatile("{\n\t.reg .pred pi, po;\n\tsetp.ne.s32 pi, %1, 0;\n\t"
+                       "bar.red.and.pred po, 1, %2, pi;\n\tselp.s32 %0, 1, 0, po;\n\t}"
+                       : "=r"(all_ok) : "r"(static_cast<int>(ok)), "n"(kLoaderThreads) : "memory");
+          if (!all_ok) {
+            for (int q = 0; q < nent; ++q) wait_row(p, ent[q][sg], st);
+            asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
           }
-          asm volatile("bar.sync 1, %0;" ::"n"(kLoaderThreads) : "memory");
-        }
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA below
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA
+        };
+        acquire_seg(0);
+        int acquired = 1;  // segments [0, acquired) are acquired
         if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
         const int pieces = nrows * 8;  // 16 B pieces per K chunk
@@ -1444,6 +1447,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
           if (sg < nseg && !segment_contig(p, st, sg, &cb[sg])) cb[sg] = -1;
         for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
           const int nk = min(kps, kc_total - kc0);
+          if (acquired < 2 && (kc0 + nk - 1) * kChunkK >= h) {  // the stage reaches segment 1
+            acquire_seg(1);
+            acquired = 2;
+          }
           const uint32_t stg = pipe.it % kStages;
           mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
           if (nk > 1) {  // several small chunks per stage: row gathers only (a 128-row box would overflow)
