@@ -269,6 +269,9 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
   return v;
 }
+#ifndef ED_POLL_NS
+#define ED_POLL_NS 32  // back-off between readiness polls
+#endif
 // A step that reads its own rows (the second contraction of a two-GEMM cell: link gate, tagger
 // output, MV-RNN p) needs only what the earlier steps of its batch publish: st.self_need.
 __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep &st) {
@@ -283,7 +286,9 @@ __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep 
              threadIdx.x, st.cell, st.out_row0, e, ld_acquire_s32(p.ready + e), need);
       __trap();
     }
-    __nanosleep(32);
+#if ED_POLL_NS > 0
+    __nanosleep(ED_POLL_NS);
+#endif
   }
 }
 // Non-blocking check of a row (same rule as wait_row).
@@ -1148,7 +1153,7 @@ __device__ __forceinline__ int step_items(const DevStep &st, int h) {
 // several K chunks into one 48 KB stage: chunk q's A at q * abytes, its B at kps * abytes + q * N * 128 B.
 // M = 128 MMAs read 128 A rows from q * abytes; rows past the tile's m are never stored.
 #ifndef ED_KPS_MAX
-#define ED_KPS_MAX 16
+#define ED_KPS_MAX 4  // measured: 4 beats 1, 2, 3 and 16 on cfg2 / cfg3 / cfg5 (r01t A/B)
 #endif
 __device__ __forceinline__ int step_kps(const DevStep &st, int kc_total, uint32_t *abytes) {
   if (st.cell == kCellMvMat) { *abytes = kAStage; return 1; }
