@@ -584,6 +584,9 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
   const int lane = threadIdx.x & 31;
   const long gw = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  float bv[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) bv[c] = c < C ? __ldg(bias + c) : 0.f;
   for (long i = gw; i < st.m; i += nw) {
     const int e = slot_entry(st, p.idx, 0, static_cast<int>(i));
     wait_row(p, e, st);
@@ -606,7 +609,9 @@ __device__ void simt_linear_out(const KParams &p, const DevStep &st) {
     }
     if (lane == 0) {
       float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];  // sink: no readiness to publish
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < C) y[c] = acc[c] + bv[c];  // sink: no readiness to publish (bias loaded up front)
     }
   }
 }
@@ -621,6 +626,12 @@ __device__ void linear_out_rows_bf16(const KParams &p, const DevStep &st, long i
   const int lane = threadIdx.x & 31;
   const int nch = h / 8;                 // 16 B chunks per row
   const int cpl = (nch + 31) / 32;       // chunks per lane (<= 4 for h <= 1024)
+  // bias first, all classes at once: loaded inside the store loop below, each class's load waited
+  // for the previous class's store (one L2 round trip per class, ~6 us per 24-row item; staging
+  // the bias in shared memory does not help: the loads still order behind the stores)
+  float bv[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) bv[c] = c < C ? __ldg(bias + c) : 0.f;
   uint4 v[2][4];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -671,7 +682,9 @@ __device__ void linear_out_rows_bf16(const KParams &p, const DevStep &st, long i
     const long i = i0 + r;
     if (lane == 0 && i < st.m) {
       float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
-      for (int c = 0; c < C; ++c) y[c] = acc[c] + bias[c];  // sink: no readiness to publish
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < C) y[c] = acc[c] + bv[c];  // sink: no readiness to publish (bias loaded up front)
     }
   }
 }

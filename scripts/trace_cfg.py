@@ -26,11 +26,16 @@ print("phases rel. to previous step end (ns): reached, rows-ready, A-issued, MMA
 for s in range(nb):
     base = end[s]
     rel = lambda k: int(t[s, k] - base) if t[s, k] else None
-    print(s, len(sched[min(s, len(sched) - 1)][1]), [rel(k) for k in (0, 1, 2, 3, 4, 6, 5)], "|", int(ts[s + 1] - base))
+    print(s, len(sched[min(s, len(sched) - 1)][1]), [rel(k) for k in (0, 1, 2, 3, 4, 6, 5)], "|", int(ts[s + 1] - base),
+          " epi loop/fence/publish:", [rel(k) for k in (7, 8, 9)])
 
 # per-CTA SIMT (last step) phases: entered, passed the CTA barrier, items done (rel. to previous step end)
 base = end[nb - 1]
-rows = [(c, int(pc[c, 0] - base), int(pc[c, 1] - base), int(pc[c, 2] - base)) for c in range(148) if pc[c, 0]]
+rows = [(c, int(pc[c, 0] - base), int(pc[c, 1] - base), int(pc[c, 2] - base)) for c in range(148) if pc[c, 1]]
 rows.sort(key=lambda r: -r[3])
 print("last step per CTA (cta, enter, synced, done) slowest first:", rows[:12])
 print("median enter/synced/done:", [int(np.median([r[k] for r in rows])) for k in (1, 2, 3)])
+it = [(c, int(pc[c, 1] - base), int(pc[c, 0] - base), int(pc[c, 3] - base) if pc[c, 3] else None, int(pc[c, 2] - base)) for c in range(148) if pc[c, 1]]
+it.sort(key=lambda r: -r[4])
+print("per CTA (cta, synced, item1 done, item2 done, all done) slowest first:", it[:16])
+print("fastest:", it[-6:])
