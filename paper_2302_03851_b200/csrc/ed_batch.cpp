@@ -390,6 +390,13 @@ static ed_status_t lower(ed_plan_t *pl) {
         if (mt * ((h + u - 1) / u) <= 148) st.units = u;
     }
     st.n_col_tiles = st.units > 0 ? (h + st.units - 1) / st.units : 0;
+    if (ot.cell_kind == ED_CELL_LINEAR_OUT && pl->dtype == ED_BF16) {
+      // bf16 output linear on the tensor cores: one N = 16 column tile (C <= 16 classes, rows >= C
+      // of the packed W_O are zero); units = C, gates = 1
+      st.gates = 1;
+      st.units = ot.out_dim;
+      st.n_col_tiles = 1;
+    }
     st.nslots = std::min(ot.num_slots, ed::kMaxSlotsDev);
     std::vector<int32_t> slot_entries[ed::kMaxSlotsDev];
     for (int j = 0; j < st.nslots; ++j) {

@@ -858,7 +858,7 @@ struct Pipe {
 };
 
 __device__ __forceinline__ bool is_umma_cell(int cell) {
-  return cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
+  return cell == ED_CELL_LINEAR_OUT || cell == ED_CELL_TREELSTM_LEAF || cell == ED_CELL_TREELSTM_INTERNAL || cell == ED_CELL_TREEGRU_LEAF ||
          cell == ED_CELL_TREEGRU_INTERNAL || cell == ED_CELL_TREEFC_INTERNAL || cell == ED_CELL_LSTM ||
          cell == ED_CELL_LATTICE_CHAR || cell == ED_CELL_LATTICE_WORD || cell == kCellLatticeLink ||
          cell == ED_CELL_LATTICEGRU_CHAR || cell == ED_CELL_LATTICEGRU_WORD ||
@@ -899,6 +899,10 @@ __device__ __forceinline__ void build_row_table(const KParams &p, const DevStep 
 
 // Hidden units of column tile ct (the last tile of a row may be narrower: h need not divide by U).
 __device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { return min(st.units, h - ct * st.units); }
+// MMA N of a column tile: G * units, or 16 for the output linear (C <= 16 classes, zero-padded W_O)
+__device__ __forceinline__ int tile_cols(const DevStep &st, int h, int ct) {
+  return st.cell == ED_CELL_LINEAR_OUT ? 16 : st.gates * tile_units(st, h, ct);
+}
 
 __device__ __forceinline__ float f4get(const float4 &v, int k) {
   return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
@@ -1112,6 +1116,28 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   }
 }
 
+// Epilogue of one 128-row tile of the output linear y = W_O h + b (fp32 logits, a sink: nothing
+// reads Y, so nothing is published): tcgen05.ld of the 16 accumulator columns, bias, C stores.
+__device__ __forceinline__ void linear_out_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
+                                                    uint32_t parity, int row_tile, int r) {
+  const int i = row_tile * kTileM + r;
+  const int C = st.units;
+  const float *bias = step_b(p, st);
+  float bv[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) bv[c] = c < C ? __ldg(bias + c) : 0.f;
+  mbar_wait(tfull_bar, parity);
+  tc_fence_after();
+  float v[16];
+  tmem_ld16(tacc, v);
+  tmem_wait_ld();
+  if (i >= st.m) return;
+  float *y = p.Y + static_cast<size_t>(st.out_row0 + i) * p.ycols;
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (c < C) y[c] = v[c] + bv[c];
+}
+
 // Epilogue of one 128 x units tile of the MV-RNN matrix product: rows R = row_tile * 128 + r of the
 // batch's m * h rows of P^T (node i = R / h, matrix row R % h), stored bf16 into the node's Mx block.
 // A warp's 32 rows belong to one node (h % 64 == 0): lane 0 publishes 32 x units elements.
@@ -1172,7 +1198,7 @@ __device__ __forceinline__ int step_kps(const DevStep &st, int kc_total, uint32_
   if (st.cell == kCellMvMat) { *abytes = kAStage; return 1; }
   const int rows = min(kTileM, (st.m + 7) & ~7);
   *abytes = static_cast<uint32_t>(rows) * 128u;
-  const int bb = st.gates * st.units * 128;
+  const int bb = (st.cell == ED_CELL_LINEAR_OUT ? 16 : st.gates * st.units) * 128;
   // small tiles: the 48 KB stage is cut as [A_0 .. A_{k-1} | B_0 .. B_{k-1}], k = 48 KB / (A + B chunk)
   const int k = *abytes < static_cast<uint32_t>(kAStage) ? kStageBytes / (static_cast<int>(*abytes) + bb) : 1;
   return max(1, min(min(k, kc_total), ED_KPS_MAX));
@@ -1255,7 +1281,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       if (tid == 0) stamp_step(p, s);
       continue;
     }
-    const int ncols = st.gates * st.units;
+    const int ncols = st.cell == ED_CELL_LINEAR_OUT ? 16 : st.gates * st.units;
     const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
     uint32_t abytes = kAStage;
     const int kps = step_kps(st, kc_total, &abytes);
@@ -1264,7 +1290,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     if (warp < 4) {
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
-      const bool bias_smem = bsrc != nullptr && st.gates * h * 4 <= kBiasBytes;
+      const bool bias_smem = bsrc != nullptr && st.cell != ED_CELL_LINEAR_OUT && st.gates * h * 4 <= kBiasBytes;
       if (bias_smem) {  // 16 B cp.async per piece: no register staging, all pieces in flight at once
         const uint32_t sb = smem_u32(sbias);
         for (int q = tid; q < st.gates * h / 4; q += kEpiThreads) cp_async16(sb + 16u * q, bsrc + 4 * q);
@@ -1305,6 +1331,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvMat:
             mv_mat_epilogue(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid); break;
+          case ED_CELL_LINEAR_OUT:
+            linear_out_epilogue(p, st, tacc, tfull + acc, par, row_tile, tid); break;
           default:
             umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
         }
@@ -1319,7 +1347,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- MMA issuer ----------------
       for (int t = t0; t < T; t += G) {
         const uint32_t acc = pipe.ti & 1u;
-        const uint32_t idesc = idesc_bf16(st.gates * tile_units(st, h, t % st.n_col_tiles));
+        const uint32_t idesc = idesc_bf16(tile_cols(st, h, t % st.n_col_tiles));
         // the whole warp walks the loop (warp-uniform operands); one elected lane issues
         mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
         tc_fence_after();
@@ -1349,10 +1377,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     } else if (warp == 5) {
       // ---------------- weight (B) loader: runs ahead across steps (weights are static) -----------
       const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
-      const size_t ntot = static_cast<size_t>(st.gates) * h;
+      const size_t ntot = st.cell == ED_CELL_LINEAR_OUT ? 16 : static_cast<size_t>(st.gates) * h;
       for (int t = t0; t < T; t += G) {  // warp-converged; one elected lane issues
         const int col_tile = t % st.n_col_tiles;
-        const uint32_t nb = static_cast<uint32_t>(st.gates * tile_units(st, h, col_tile)) * 128u;
+        const uint32_t nb = static_cast<uint32_t>(tile_cols(st, h, col_tile)) * 128u;
         for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
           const int nk = min(kps, kc_total - kc0);
           const uint32_t stg = pipe.it % kStages;
@@ -1530,7 +1558,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
 // bf16 tensor-core layout of a logical [G*h, K] matrix: [K/64][G*h][64] bf16, packed row p holds
 // logical row g*h + j with p = (j/16)*(G*16) + g*16 + j%16 (gate-interleaved in 16-unit groups),
 // and each 8-row x 128 B atom is 128B-swizzled (16 B chunk c of row r stored at c ^ (r & 7)).
-__global__ void pack_umma_kernel(const float *src, __nv_bfloat16 *dst, int G, int h, int K) {
+__global__ void pack_umma_kernel(const float *src, __nv_bfloat16 *dst, int G, int h, int K, int valid_rows) {
   const long N = static_cast<long>(G) * h;
   const long total = N * K;
   for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
@@ -1541,7 +1569,8 @@ __global__ void pack_umma_kernel(const float *src, __nv_bfloat16 *dst, int G, in
     const int within = static_cast<int>(pr % (G * 16));
     const int g = within / 16;
     const long j = grp * 16 + within % 16;
-    const float v = src[(static_cast<long>(g) * h + j) * K + k];
+    const long lr = static_cast<long>(g) * h + j;  // logical row (rows >= valid_rows are zero padding)
+    const float v = lr < valid_rows ? src[lr * K + k] : 0.0f;
     const int kc = k / 64, kk = k % 64;
     const int ch = kk / 8, e = kk % 8;
     const long byte = (static_cast<long>(kc) * N + pr) * 128 + ((ch ^ static_cast<int>(pr & 7)) * 16) + e * 2;
@@ -1605,6 +1634,7 @@ static void logical_shape(int cell, int h, int out_dim, int which, long *rows, l
 int64_t packed_bytes(int cell, int hidden, int out_dim, int dtype, int which) {
   long rows = 0, cols = 0;
   logical_shape(cell, hidden, out_dim, which, &rows, &cols);
+  if (cell == ED_CELL_LINEAR_OUT && dtype == ED_BF16) return 16 * cols * 2;  // UMMA layout, N = 16 (zero rows >= C)
   if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) return rows * cols * 4;
   return rows * cols * (dtype == ED_BF16 ? 2 : 4);
 }
@@ -1623,6 +1653,12 @@ int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const f
       pack_mat_transpose_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), out_dim, hidden);
     else
       pack_mat_transpose_kernel<float><<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), out_dim, hidden);
+  } else if (cell == ED_CELL_LINEAR_OUT && dtype == ED_BF16) {
+    if (hidden % 64 != 0) return static_cast<int>(cudaErrorInvalidValue);
+    const long total16 = 16 * cols;
+    const int b16 = static_cast<int>((total16 + threads - 1) / threads);
+    pack_umma_kernel<<<b16, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), 1, 16, static_cast<int>(cols),
+                                             static_cast<int>(rows));
   } else if (cell == ED_CELL_LINEAR_OUT || (cell == ED_CELL_TAGGER && which == 1)) {
     copy_f32_kernel<<<blocks, threads, 0, s>>>(src, static_cast<float *>(dst), total);
   } else if (dtype == ED_BF16 && umma_cell_host(cell) &&
@@ -1630,7 +1666,7 @@ int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const f
     if (hidden % 64 != 0) return static_cast<int>(cudaErrorInvalidValue);
     const int G = which == 0 ? cell_gates(cell) : 1;  // link gate W_l: one gate block
     pack_umma_kernel<<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), G, hidden,
-                                                static_cast<int>(cols));
+                                                static_cast<int>(cols), static_cast<int>(rows));
   } else if (dtype == ED_BF16) {
     pack_transpose_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), rows, cols);
   } else {
