@@ -232,9 +232,16 @@ int64_t ed_packed_bytes(int32_t cell_kind, int32_t hidden, int32_t out_dim, int3
 ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, int32_t dtype, int32_t which,
                             const float *logical_dev, void *packed_dev, void *stream);
 
-/* Execute the plan: one persistent cooperative kernel on `stream`.  The first execute on a
- * given workspace also uploads the step table (async H2D) and zeroes the zero row.  Results:
- * node records in the workspace row buffers (offsets in ed_plan_info_t) and io->out_root. */
+/* Execute the plan: one persistent cooperative kernel on `stream`, nothing else (no memsets).
+ * The first execute of a plan on a workspace binds them: it uploads the plan's static part (step
+ * table, index arrays, readiness targets, a binding nonce in the workspace header; async H2D) and
+ * zeroes the readiness counters, the zero row and the staged rows.  Later executes reuse the
+ * binding (readiness counters are monotonic across launches).  The workspace contents must
+ * persist between executes; before freeing or reusing the memory for anything else call
+ * ed_workspace_release (a launch on a workspace whose header no longer holds the nonce traps).
+ * Results: node records in the workspace row buffers (offsets in ed_plan_info_t) and, when
+ * io->out_root is non-null, the instance outputs out_root[num_instances x hidden] (plan dtype),
+ * written by the epilogues that produce the root rows. */
 ed_status_t ed_execute(ed_plan_t *plan, const ed_weights_t *weights, const ed_io_t *io, void *workspace,
                        size_t workspace_bytes, void *stream);
 
@@ -244,6 +251,10 @@ int64_t ed_plan_upload_bytes(const ed_plan_t *plan);
 
 /* Number of kernels ed_execute launches (for launch accounting). */
 int32_t ed_execute_launch_count(const ed_plan_t *plan);
+
+/* Forget the plan binding of a workspace (call before freeing or reusing its memory; a later
+ * execute on the same address binds again).  Host-only, no device work; ED_E_INVALID_ARG on null. */
+ed_status_t ed_workspace_release(const void *workspace);
 
 /* ---------------------------------------------------------------------------------------------
  * Learning the FSM (PAPER §2.3 "Using RL to Learn the FSM"; §5.3): tabular

@@ -108,9 +108,15 @@ cudaError_t upload_async(void *dst, const void *src, size_t n, cudaStream_t s) {
 
 // Which plan's static part currently sits in which workspace (a workspace can be shared by
 // several plans; the step table is re-uploaded whenever the owner changes).
+struct WsBinding {
+  const void *plan = nullptr;
+  uint64_t nonce = 0;  // written into the workspace header at binding, checked by every launch
+  uint32_t seq = 0;    // launches since the binding (readiness counters are monotonic)
+};
 struct WsRegistry {
   std::mutex mu;
-  std::map<const void *, const void *> owner;  // workspace -> plan
+  std::map<const void *, WsBinding> owner;  // workspace -> binding
+  uint64_t next_nonce = 0x5EDB000000000001ull;
 };
 WsRegistry &ws_registry() {
   static WsRegistry r;
@@ -151,6 +157,7 @@ struct ed_plan_s {
   int64_t contig = 0, gather = 0, copy_bytes = 0, copy_kernels = 0;
   bool staging = true;      // bf16: stage gathered cell operands into contiguous blocks
   int64_t op_rows = 0;      // staged operand rows appended to H (rows V+1 ..)
+  int32_t ext_root_off = 0, num_ext_roots = 0;  // instances whose output is an input lookup
   int64_t staged = 0, staged_bytes = 0;
   int64_t dst_base = 0;     // idx offset of dst_off[V + 2] (then the copy destinations)
   double plan_us = 0, sched_us = 0, layout_us = 0, validate_us = 0, lower_us = 0;
@@ -522,7 +529,23 @@ static ed_status_t lower(ed_plan_t *pl) {
       pl->steps.push_back(s2);
     }
   }
-  // copies of every result row into staged operand blocks (CSR over rows 0..V), appended to idx
+  // instance outputs: the epilogue producing an instance's root row also stores it into
+  // out_root[instance] (a copy entry -1 - instance); roots that are input lookups are copied by CTA 0
+  std::vector<int32_t> ext_roots;
+  for (int i = 0; i < pl->ninst; ++i) {
+    const int32_t r = pl->roots[i];
+    if (r >= 0)
+      stage_pairs.emplace_back(pl->row_of_node[r], -1 - i);
+    else {
+      ext_roots.push_back(i);
+      ext_roots.push_back(-1 - r);
+    }
+  }
+  pl->ext_root_off = static_cast<int32_t>(pl->idx.size());
+  pl->num_ext_roots = static_cast<int32_t>(ext_roots.size() / 2);
+  pl->idx.insert(pl->idx.end(), ext_roots.begin(), ext_roots.end());
+  // copies of every result row into staged operand blocks and instance outputs (CSR over rows
+  // 0..V), appended to idx
   {
     std::vector<int32_t> cnt(V + 2, 0);
     for (const auto &pr : stage_pairs) ++cnt[pr.first + 1];
@@ -553,7 +576,7 @@ static ed_status_t lower(ed_plan_t *pl) {
   const int64_t rows = V + 1;
   const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
   size_t off = 0;
-  pl->off_bar = off; off += 256 + 256 * 1024;  // counter + per-CTA flags (256 B apart)
+  pl->off_bar = off; off += 256;  // header: binding nonce (8 B)
   const size_t nsteps = pl->steps.size();
   pl->off_ts = off; off = align_up(off + 8 * (nsteps + 1), 256);
   pl->off_steps = off; off = align_up(off + sizeof(ed::DevStep) * nsteps, 256);
@@ -578,12 +601,13 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->off_u = off; if (pl->need_mv) off = align_up(off + elt * rows * 2 * h, 1024);
   pl->off_m = off; if (pl->need_mv) off = align_up(off + elt * rows * h * h, 1024);
   pl->ws_bytes = off;
-  // host blob mirrors [ts .. roots] so one async H2D uploads the static part
-  pl->blob.assign(pl->off_ready - pl->off_ts, 0);
-  std::memcpy(pl->blob.data() + (pl->off_steps - pl->off_ts), pl->steps.data(), sizeof(ed::DevStep) * nsteps);
-  if (!pl->idx.empty()) std::memcpy(pl->blob.data() + (pl->off_idx - pl->off_ts), pl->idx.data(), 4 * pl->idx.size());
-  if (pl->ninst) std::memcpy(pl->blob.data() + (pl->off_roots - pl->off_ts), pl->root_rows.data(), 4 * pl->ninst);
-  std::memcpy(pl->blob.data() + (pl->off_target - pl->off_ts), pl->target.data(), 4 * pl->target.size());
+  // host blob mirrors [header .. target] so one async H2D uploads the static part (the header's
+  // nonce is filled in per binding)
+  pl->blob.assign(pl->off_ready - pl->off_bar, 0);
+  std::memcpy(pl->blob.data() + (pl->off_steps - pl->off_bar), pl->steps.data(), sizeof(ed::DevStep) * nsteps);
+  if (!pl->idx.empty()) std::memcpy(pl->blob.data() + (pl->off_idx - pl->off_bar), pl->idx.data(), 4 * pl->idx.size());
+  if (pl->ninst) std::memcpy(pl->blob.data() + (pl->off_roots - pl->off_bar), pl->root_rows.data(), 4 * pl->ninst);
+  std::memcpy(pl->blob.data() + (pl->off_target - pl->off_bar), pl->target.data(), 4 * pl->target.size());
   return ED_OK;
 }
 
@@ -849,7 +873,7 @@ void ed_plan_destroy(ed_plan_t *pl) {
     WsRegistry &reg = ws_registry();
     std::lock_guard<std::mutex> lk(reg.mu);
     for (auto it = reg.owner.begin(); it != reg.owner.end();)
-      it = (it->second == pl) ? reg.owner.erase(it) : std::next(it);
+      it = (it->second.plan == pl) ? reg.owner.erase(it) : std::next(it);
   }
   delete pl;
 }
@@ -873,6 +897,14 @@ ed_status_t ed_pack_weights(int32_t cell_kind, int32_t hidden, int32_t out_dim, 
 
 int32_t ed_execute_launch_count(const ed_plan_t *pl) { return pl ? 1 : 0; }  // one persistent kernel
 
+ed_status_t ed_workspace_release(const void *ws) {
+  if (!ws) return fail(ED_E_INVALID_ARG, "null workspace");
+  WsRegistry &reg = ws_registry();
+  std::lock_guard<std::mutex> lk(reg.mu);
+  reg.owner.erase(ws);
+  return ED_OK;
+}
+
 ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, void *ws, size_t ws_bytes,
                        void *stream) {
   if (!pl || !w) return fail(ED_E_INVALID_ARG, "null argument");
@@ -888,15 +920,25 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t *base = static_cast<uint8_t *>(ws);
   bool need_upload;
+  uint64_t nonce = 0;
+  uint32_t seq = 0;
   {
     WsRegistry &reg = ws_registry();
     std::lock_guard<std::mutex> lk(reg.mu);
     auto it = reg.owner.find(ws);
-    need_upload = (it == reg.owner.end() || it->second != pl);
+    need_upload = (it == reg.owner.end() || it->second.plan != pl);
+    if (!need_upload) {
+      nonce = it->second.nonce;
+      seq = ++it->second.seq;
+    } else {
+      nonce = reg.next_nonce++;
+    }
   }
   if (need_upload) {
-    cudaError_t ce = upload_async(base + pl->off_ts, pl->blob.data(), pl->blob.size(), s);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_bar, 0, pl->off_ts - pl->off_bar, s);  // barrier flags
+    // bind: upload the static part with the binding nonce in its header, zero the readiness counters
+    std::memcpy(pl->blob.data(), &nonce, sizeof(nonce));
+    cudaError_t ce = upload_async(base + pl->off_bar, pl->blob.data(), pl->blob.size(), s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_ready, 0, 4 * static_cast<size_t>(pl->V + 1), s);
     if (ce == cudaSuccess) {
       const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
       // zero row V and the staged rows (zero-state entries are never written by a producer)
@@ -913,7 +955,10 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
     if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
     WsRegistry &reg = ws_registry();
     std::lock_guard<std::mutex> lk(reg.mu);
-    reg.owner[ws] = pl;
+    WsBinding &b = reg.owner[ws];
+    b.plan = pl;
+    b.nonce = nonce;
+    b.seq = seq = 1;
   }
   if (pl->grid == 0) {
     e = ed::persistent_grid(pl->dtype, &pl->grid);
@@ -930,16 +975,15 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   p.X = pl->need_x ? reinterpret_cast<float *>(base + pl->off_x) : nullptr;
   p.U = pl->need_mv ? base + pl->off_u : nullptr;
   p.Mx = pl->need_mv ? base + pl->off_m : nullptr;
-  p.bar = reinterpret_cast<unsigned int *>(base + pl->off_bar);
+  p.hdr = reinterpret_cast<const unsigned long long *>(base + pl->off_bar);
+  p.nonce = nonce;
+  p.seq = seq;
+  p.ext_root_off = pl->ext_root_off;
+  p.num_ext_roots = pl->num_ext_roots;
   p.ts = reinterpret_cast<unsigned long long *>(base + pl->off_ts);
   p.ready = reinterpret_cast<int *>(base + pl->off_ready);
   p.target = reinterpret_cast<const int *>(base + pl->off_target);
   p.dst_off = p.idx + pl->dst_base;
-  {  // per launch: readiness counters and step stamps start from zero
-    cudaError_t ce = cudaMemsetAsync(p.ready, 0, 4 * static_cast<size_t>(pl->V + 1), s);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(p.ts, 0, 8 * (pl->steps.size() + 1), s);
-    if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("memset: ") + cudaGetErrorString(ce));
-  }
   p.out_root = io ? io->out_root : nullptr;
   p.trace = io ? reinterpret_cast<unsigned long long *>(io->trace) : nullptr;
   p.num_steps = static_cast<int32_t>(pl->steps.size());
@@ -949,8 +993,6 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   p.ycols = static_cast<int32_t>(pl->y_cols);
   p.num_inst = pl->ninst;
   p.root_wset = pl->types[0].weight_set;
-  p.launch_id = (++pl->launches) & 0xFFFFu;
-  if (p.launch_id == 0) p.launch_id = (++pl->launches) & 0xFFFFu;
   for (int k = 0; k < w->num_sets; ++k) {
     const ed_weight_set_t &ws_ = w->sets[k];
     p.w[k] = ed::DevWeightSet{ws_.W, ws_.b, ws_.W2, ws_.b2, ws_.emb, ws_.emb2, ws_.mat, ws_.emb_rows, ws_.emb2_rows};

@@ -77,12 +77,15 @@ struct alignas(64) KParams {
   float *X;                   // [rows x hidden] (lattice link gates) or null
   void *U;                    // [rows x 2 hidden] (MV-RNN matvec results [B a; A b]) or null
   void *Mx;                   // [rows x hidden x hidden] (MV-RNN node matrices, transposed) or null
-  unsigned int *bar;          // grid barrier counter (zeroed before launch)
-  unsigned long long *ts;     // [num_steps + 1]
+  const unsigned long long *hdr;  // workspace header: the binding nonce written when the plan was uploaded
+  unsigned long long nonce;   // expected header value (a stale or replaced workspace traps)
+  unsigned long long *ts;     // [num_steps + 1] (max of %globaltimer: monotonic, never zeroed)
   void *out_root;             // [num_inst x hidden] or null
   unsigned long long *trace;  // [num_steps x 64] phase stamps of CTA 0, or null
-  const int32_t *dst_off;     // [rows + 1] staged-operand copies of each result row (CSR into idx)
-  int *ready;                 // [rows] hidden units published per row (zeroed every launch)
+  const int32_t *dst_off;     // [rows + 1] copies of each result row (CSR into idx): entry >= 0 a staged
+                              // H row, entry < 0 the instance output out_root[-1 - entry]
+  int *ready;                 // [rows] units published per row, monotonic over launches: after launch
+                              // k a row holds k * target (mod 2^32); zeroed only when the workspace is bound
   const int *target;          // [rows] units a row holds when final (sum of step_contrib)
   int32_t num_steps;
   int32_t hidden;
@@ -91,8 +94,9 @@ struct alignas(64) KParams {
   int32_t ycols;
   int32_t num_inst;
   int32_t root_wset;
-  uint32_t launch_id;          // distinguishes barrier flags of successive launches
-  int32_t pad2[2];
+  uint32_t seq;               // launches of this plan on this workspace binding, 1, 2, ...
+  int32_t ext_root_off;       // idx offset of (instance, external id) pairs of instances whose
+  int32_t num_ext_roots;      // output is an input lookup (no op produces it)
   DevWeightSet w[kMaxWeightSets];
 };
 

@@ -220,40 +220,6 @@ __device__ __forceinline__ uint32_t idesc_bf16(int n) {
          (static_cast<uint32_t>(kTileM >> 4) << 24);
 }
 
-// Grid-wide barrier between dependent batches.  Arrivals: one acq_rel atomic per CTA on a counter;
-// the last arriver's warp 0 publishes the epoch to a per-CTA flag (one 256 B line per CTA, so the
-// waiting CTAs poll 148 different L2 lines instead of hammering one).  Flag value =
-// launch_id << 16 | epoch, so flags left by earlier launches never match.
-__device__ __forceinline__ void grid_sync(unsigned int *bar, unsigned int launch_id, unsigned int &epoch) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    ++epoch;
-    const unsigned int target = epoch * gridDim.x;
-    const unsigned int want = (launch_id << 16) | epoch;
-    unsigned int *flags = bar + 64;
-    unsigned int old = 0;
-    if (threadIdx.x == 0)  // acq_rel: releases this CTA's writes, acquires every earlier arrival
-      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old == target - 1) {
-      // last arriver: warp 0 publishes the epoch to every CTA's flag line (release pattern:
-      // the acquire of the RMW chain, then a fence, then relaxed stores)
-      __threadfence();
-      for (unsigned int c = threadIdx.x; c < gridDim.x; c += 32)
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + c * 64), "r"(want) : "memory");
-    } else if (threadIdx.x == 0) {
-      unsigned int v, spins = 0;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + blockIdx.x * 64) : "memory");
-        if (v == want) break;
-        if (++spins > (1u << 26)) __trap();
-        __nanosleep(32);
-      }
-    }
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -261,8 +227,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 // ---- dataflow readiness (replaces per-batch grid barriers) ----
 // ready[row] counts units written to the row by finished device steps; target[row] = the sum of
-// step_contrib over the device steps that write it (h per row-vector result, h*h for a matrix).  A consumer acquires ready[row] >= target[row] before reading
-// the row; a producer publishes with a release-add after its stores.  Rows are only produced by
+// step_contrib over the device steps that write it (h per row-vector result, h*h for a matrix).
+// A consumer acquires ready[row] - base >= target[row] before reading the row, base = (seq - 1) *
+// target[row] (mod 2^32: the counters are never reset between launches, so no memset precedes a
+// launch); a producer publishes with a release-add after its stores.  Rows are only produced by
 // earlier device steps and every warp walks the steps in order, so waiting cannot deadlock.
 __device__ __forceinline__ int ld_acquire_s32(const int *a) {
   int v;
@@ -274,16 +242,20 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
 #endif
 // A step that reads its own rows (the second contraction of a two-GEMM cell: link gate, tagger
 // output, MV-RNN p) needs only what the earlier steps of its batch publish: st.self_need.
+__device__ __forceinline__ int ready_since_launch(const KParams &p, int e, int tgt) {
+  return static_cast<int>(static_cast<uint32_t>(ld_acquire_s32(p.ready + e)) - (p.seq - 1u) * static_cast<uint32_t>(tgt));
+}
 __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep &st) {
   if (e < 0 || e >= p.rows) return;  // external rows are static
-  int need = __ldg(p.target + e);
+  const int tgt = __ldg(p.target + e);
+  int need = tgt;
   if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
   if (need <= 0) return;
   unsigned spins = 0;
-  while (ld_acquire_s32(p.ready + e) < need) {
+  while (ready_since_launch(p, e, tgt) < need) {
     if (++spins > (1u << 26)) {  // watchdog: report the stuck dependency, then abort the launch
       printf("ed_batch watchdog: block %d thread %d cell %d out_row0 %d row %d ready %d need %d\n", blockIdx.x,
-             threadIdx.x, st.cell, st.out_row0, e, ld_acquire_s32(p.ready + e), need);
+             threadIdx.x, st.cell, st.out_row0, e, ready_since_launch(p, e, tgt), need);
       __trap();
     }
 #if ED_POLL_NS > 0
@@ -294,12 +266,40 @@ __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep 
 // Non-blocking check of a row (same rule as wait_row).
 __device__ __forceinline__ bool row_ready(const KParams &p, int e, const DevStep &st) {
   if (e < 0 || e >= p.rows) return true;
-  int need = __ldg(p.target + e);
+  const int tgt = __ldg(p.target + e);
+  int need = tgt;
   if (e >= st.out_row0 && e < st.out_row0 + st.m) need = st.self_need;
-  return need <= 0 || ld_acquire_s32(p.ready + e) >= need;
+  return need <= 0 || ready_since_launch(p, e, tgt) >= need;
 }
 __device__ __forceinline__ void publish_row(const KParams &p, int row, int units) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + row), "r"(units) : "memory");
+}
+// Row copies listed in dst_off: a staged operand row of H (d >= 0) or the instance output
+// out_root[-1 - d] (written here by the producer's epilogue, no final gather pass); null when the
+// caller passed no out_root.
+template <typename T>
+__device__ __forceinline__ T *copy_row(const KParams &p, int d) {
+  if (d >= 0) return static_cast<T *>(p.H) + static_cast<size_t>(d) * p.hidden;
+  return p.out_root ? static_cast<T *>(p.out_root) + static_cast<size_t>(-1 - d) * p.hidden : nullptr;
+}
+// Kernel prologue: the workspace must still hold the binding this launch was planned for (a freed
+// and reallocated workspace has lost its step table and readiness counters: fail loudly), and
+// instance outputs that are input lookups (no op produces them) are copied by CTA 0.
+template <typename T>
+__device__ void prologue_checks(const KParams &p) {
+  if (threadIdx.x == 0 && *p.hdr != p.nonce) {
+    printf("ed_batch: workspace binding lost (header %llx, expected %llx): call ed_workspace_release "
+           "before freeing a workspace\n", *p.hdr, p.nonce);
+    __trap();
+  }
+  if (blockIdx.x != 0 || p.num_ext_roots == 0 || p.out_root == nullptr) return;
+  const int h = p.hidden;
+  for (int q = threadIdx.x; q < p.num_ext_roots * h; q += blockDim.x) {
+    const int k = q / h, j = q % h;
+    const int inst = __ldg(p.idx + p.ext_root_off + 2 * k), id = __ldg(p.idx + p.ext_root_off + 2 * k + 1);
+    const T *tab = static_cast<const T *>(p.w[p.root_wset].emb);
+    static_cast<T *>(p.out_root)[static_cast<size_t>(inst) * h + j] = tab[static_cast<size_t>(id) * h + j];
+  }
 }
 __device__ __forceinline__ void stamp_step(const KParams &p, int s) {
   atomicMax(p.ts + s + 1, globaltimer());
@@ -528,6 +528,10 @@ __device__ __forceinline__ void cell_epilogue(const KParams &p, const DevStep &s
   }
   H[orow * h + j] = from_f<T>(hv);
   if (has_c) p.C[orow * h + j] = c;
+  for (int d = __ldg(p.dst_off + orow); d < __ldg(p.dst_off + orow + 1); ++d) {
+    T *dst = copy_row<T>(p, __ldg(p.idx + d));
+    if (dst) dst[j] = from_f<T>(hv);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -810,27 +814,13 @@ __device__ void simt_mv_mat(const KParams &p, const DevStep &st) {
   }
 }
 
-template <typename T>
-__device__ void collect_roots(const KParams &p) {
-  if (p.out_root == nullptr) return;
-  const int h = p.hidden;
-  T *out = static_cast<T *>(p.out_root);
-  const long total = static_cast<long>(p.num_inst) * h;
-  for (long q = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
-       q += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int inst = static_cast<int>(q / h), j = static_cast<int>(q % h);
-    const int r = p.root_rows[inst];
-    out[q] = entry_row<T>(p, p.w[p.root_wset], r, false)[j];
-  }
-}
-
 // ------------------------------------------------------------------------------------------------
 // fp32 persistent kernel: all SIMT
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1) ed_persistent_f32(const __grid_constant__ KParams p) {
   __shared__ float s_vec[2048];          // MV-RNN matvec operand (h <= 2048)
   __shared__ float s_red[kThreads * 4];  // MV-RNN partial sums
-  unsigned int epoch = 0;
+  prologue_checks<float>(p);
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ts[0] = globaltimer();
   for (int s = 0; s < p.num_steps; ++s) {  // dataflow: tasks wait on their input rows, no barrier
     const DevStep st = p.steps[s];
@@ -845,8 +835,6 @@ __global__ void __launch_bounds__(kThreads, 1) ed_persistent_f32(const __grid_co
     __syncthreads();
     if (threadIdx.x == 0) stamp_step(p, s);
   }
-  grid_sync(p.bar, p.launch_id, epoch);  // roots are read by any CTA
-  collect_roots<float>(p);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -944,11 +932,12 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   const float4 *cp0 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e0) * h + jb);
   const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1) * h + jb);
   const __nv_bfloat16 *Hb = static_cast<const __nv_bfloat16 *>(p.H);
-  int dbeg = 0, dend = 0, d0 = -1;  // staged-operand copies of this result row (first one in a register)
+  int dbeg = 0, dend = 0;  // copies of this result row (staged operand rows, instance output)
+  __nv_bfloat16 *cpy0 = nullptr;  // the first copy's row, resolved up front
   if (valid && CELL != kCellLatticeLink) {
     dbeg = __ldg(p.dst_off + st.out_row0 + i);
     dend = __ldg(p.dst_off + st.out_row0 + i + 1);
-    if (dbeg < dend) d0 = __ldg(p.idx + dbeg++);
+    if (dbeg < dend) cpy0 = copy_row<__nv_bfloat16>(p, __ldg(p.idx + dbeg++));
   }
   const uint4 *hp0 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e0) * h + jb);
   const uint4 *hp1 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e1) * h + jb);
@@ -1099,9 +1088,11 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       }
       const uint4 hv4 = make_uint4(packed[0], packed[1], packed[2], packed[3]);
       *reinterpret_cast<uint4 *>(H + orow * h + j0) = hv4;
-      if (d0 >= 0) *reinterpret_cast<uint4 *>(H + static_cast<size_t>(d0) * h + j0) = hv4;
-      for (int d = dbeg; d < dend; ++d)
-        *reinterpret_cast<uint4 *>(H + static_cast<size_t>(__ldg(p.idx + d)) * h + j0) = hv4;
+      if (cpy0 != nullptr) *reinterpret_cast<uint4 *>(cpy0 + j0) = hv4;
+      for (int d = dbeg; d < dend; ++d) {
+        __nv_bfloat16 *dst = copy_row<__nv_bfloat16>(p, __ldg(p.idx + d));
+        if (dst != nullptr) *reinterpret_cast<uint4 *>(dst + j0) = hv4;
+      }
     }
     if constexpr (HAS_C) {
       float *dst = (CELL == kCellLatticeLink) ? p.X : p.C;
@@ -1239,6 +1230,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  prologue_checks<__nv_bfloat16>(p);
   if (blockIdx.x == 0 && tid == 0) p.ts[0] = globaltimer();
 
   const int h = p.hidden;
@@ -1544,9 +1536,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       }
     }
   }
-  unsigned int epoch = 0;
-  grid_sync(p.bar, p.launch_id, epoch);  // every row is final: collect the instance outputs
-  collect_roots<__nv_bfloat16>(p);
   tc_fence_before();
   __syncthreads();
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
@@ -1712,8 +1701,7 @@ int persistent_grid(int dtype, int *grid) {
 
 int launch_persistent(const KParams &p, int dtype, int grid, void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(p.bar, 0, 256, s);
-  if (e != cudaSuccess) return static_cast<int>(e);
+  cudaError_t e;
   void *args[] = {const_cast<KParams *>(&p)};
   if (dtype == ED_BF16) {
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_bf16), dim3(grid), dim3(kThreadsTC), args,

@@ -121,6 +121,9 @@ def _load() -> ctypes.CDLL:
     lib.ed_execute.argtypes = [ctypes.c_void_p, _p(ed_weights_t), _p(ed_io_t), ctypes.c_void_p, ctypes.c_size_t,
                                ctypes.c_void_p]
     lib.ed_execute_launch_count.argtypes = [ctypes.c_void_p]
+    if hasattr(lib, "ed_workspace_release") or LIB_PATH.endswith("paper_2302_03851_b200/libedbatch.so"):
+        lib.ed_workspace_release.argtypes = [ctypes.c_void_p]  # (older A/B builds via ED_BATCH_LIB lack it)
+        lib.ed_workspace_release.restype = ctypes.c_int32
     lib.ed_plan_upload_bytes.argtypes = [ctypes.c_void_p]
     lib.ed_plan_upload_bytes.restype = ctypes.c_int64
     lib.ed_fsm_learn.argtypes = [_p(ed_graph_t), ctypes.c_int32, _p(ed_op_type_t), ctypes.c_int32,
@@ -389,6 +392,21 @@ class Workspace:
         self.nbytes = nbytes
         self.plan_info = plan.info
 
+    def release(self) -> None:
+        """Unbind the workspace from its plan (ed_workspace_release) and drop the memory: the next
+        allocation at this address must not inherit the binding."""
+        if getattr(self, "buf", None) is not None:
+            if hasattr(LIB, "ed_workspace_release"):
+                LIB.ed_workspace_release(ctypes.c_void_p(self.buf.data_ptr()))
+            self.buf = None
+            self.raw = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
     @property
     def ptr(self) -> int:
         return self.buf.data_ptr()
@@ -445,6 +463,16 @@ class Workspace:
 
 def ed_execute(plan: Plan, weights: DeviceWeights, workspace: Workspace, out_root: Optional[torch.Tensor] = None,
                stream=None, trace: Optional[torch.Tensor] = None) -> None:
+    info = plan.info
+    if out_root is not None:
+        want = torch.bfloat16 if info["dtype"] == ED_BF16 else torch.float32
+        if not (out_root.is_cuda and out_root.is_contiguous() and out_root.dtype == want
+                and out_root.numel() >= info["num_instances"] * info["hidden"]):
+            raise ValueError(f"out_root must be a contiguous CUDA {want} tensor with >= "
+                             f"{info['num_instances']} x {info['hidden']} elements")
+    if trace is not None and not (trace.is_cuda and trace.is_contiguous() and trace.dtype == torch.int64
+                                  and trace.numel() >= info["num_steps"] * 64 + 148 * 4):
+        raise ValueError("trace must be a contiguous CUDA int64 tensor of >= num_steps * 64 + 148 * 4 elements")
     io = ed_io_t(ctypes.c_void_p(out_root.data_ptr()) if out_root is not None else None,
                  ctypes.c_void_p(trace.data_ptr()) if trace is not None else None)
     _check(LIB.ed_execute(plan.handle, ctypes.byref(weights.struct), ctypes.byref(io),

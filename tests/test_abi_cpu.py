@@ -197,7 +197,9 @@ def test_packed_bytes():
     h = 512
     assert E.ed_packed_bytes("treelstm_internal", h, 0, "bf16", 0) == 5 * h * 2 * h * 2
     assert E.ed_packed_bytes("treelstm_leaf", h, 0, "fp32", 0) == 3 * h * h * 4
-    assert E.ed_packed_bytes("linear_out", h, 5, "bf16", 0) == 5 * h * 4
+    # bf16 output linear: UMMA layout of a zero-padded N = 16 tile; fp32: [C][h] fp32
+    assert E.ed_packed_bytes("linear_out", h, 5, "bf16", 0) == 16 * h * 2
+    assert E.ed_packed_bytes("linear_out", h, 5, "fp32", 0) == 5 * h * 4
 
 
 def test_empty_and_degenerate_graphs():

@@ -215,3 +215,39 @@ def test_small_contiguous_tiles_with_single_chunk_last_stage(h):
     contiguous operand must gather it, not load a 128-row TMA box over the stage's B region
     (h = 192: 6 K chunks = stages of 5 + 1 for 8-row tiles)."""
     _check(W.bilstm(8, (6, 14), h, "bf16", cfg=71, with_tagger=False))
+
+
+def test_repeated_launches_rebinding_and_two_workspaces():
+    """Readiness counters are monotonic over launches (no per-launch memset): many executes of one
+    plan, a second workspace bound in between, and a released + rebound workspace all give the
+    bitwise-same node records and instance outputs as the first launch."""
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.treelstm(40, (1, 30), 128, "bf16", cfg=72)
+    plan, w, ws, out = run_gpu(wl)
+    ref_h, ref_out = ws.H().clone(), out.clone()
+    ws2 = E.Workspace(plan)
+    out2 = torch.zeros_like(out)
+    for k in range(7):
+        E.ed_execute(plan, w, ws if k % 2 == 0 else ws2, out if k % 2 == 0 else out2)
+    torch.cuda.synchronize()
+    assert torch.equal(ws.H(), ref_h) and torch.equal(out, ref_out)
+    assert torch.equal(ws2.H()[: ref_h.shape[0]], ref_h) and torch.equal(out2, ref_out)
+    ws2.release()
+    ws3 = E.Workspace(plan)  # may reuse ws2's address: must bind afresh
+    out3 = torch.zeros_like(out)
+    for _ in range(3):
+        E.ed_execute(plan, w, ws3, out3)
+    torch.cuda.synchronize()
+    assert torch.equal(out3, ref_out)
+    err = compare(wl, plan, ws3, out3)
+    assert all(v <= TOL[wl.dtype] for v in err.values()), err
+
+
+def test_out_root_is_validated():
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.treelstm(4, (2, 6), 64, "bf16", cfg=73)
+    plan, w, ws, out = run_gpu(wl)
+    with pytest.raises(ValueError):
+        E.ed_execute(plan, w, ws, out.float())
+    with pytest.raises(ValueError):
+        E.ed_execute(plan, w, ws, out[:2])
