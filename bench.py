@@ -33,6 +33,7 @@ METRICS = {"cfg3": METRIC,
            "cfg1": "instances/sec TreeLSTM h=32 (cfg1: 8 random trees, fp32) per step, whole job",
            "cfg2": "instances/sec BiLSTM-tagger h=256 (cfg2: 64 sequences, bf16) per step, whole job",
            "cfg5": "instances/sec LatticeLSTM h=256 (cfg5: 512 lattices, bf16) per step, whole job",
+           "cfg5_h512": "instances/sec LatticeLSTM h=512 (512 lattices, bf16; BASELINE metric, A-24) per step, whole job",
            "cfg5_gru": "instances/sec LatticeGRU h=256 (512 lattices, bf16) per step, whole job",
            "cfg4_treefc": "instances/sec TreeFC h=512 (cfg4: 1024 trees, bf16) per step, whole job",
            "cfg4_mvrnn": "instances/sec MV-RNN h=512 (cfg4: 1024 trees, bf16) per step, whole job"}
@@ -43,6 +44,7 @@ CONFIGS = {
     "cfg1": "cfg1 TreeLSTM h=32, 8 random trees (leaves U[2,16]), fp32",
     "cfg2": "cfg2 BiLSTM tagger h=256, 64 sequences of length U[10,50], bf16",
     "cfg5": "cfg5 LatticeLSTM h=256, 512 character lattices (chars U[10,50], word p=0.3), bf16",
+    "cfg5_h512": "cfg5 LatticeLSTM h=512 (the metric's hidden size, A-24), 512 character lattices (chars U[10,50], word p=0.3), bf16",
     "cfg5_gru": "cfg5 LatticeGRU h=256 (P:294, A-27), 512 character lattices (chars U[10,50], word p=0.3), bf16",
     "cfg4_treefc": "cfg4 TreeFC h=512, 1024 random trees (leaves U[5,40]), bf16",
     "cfg4_mvrnn": "cfg4 MV-RNN h=512, 1024 random trees (leaves U[5,40], 1024 word vectors + matrices), bf16",
@@ -78,6 +80,8 @@ def _weak_workload(name: str, rank: int):
         return W.bilstm(64, (10, 50), 256, "bf16", 2 + 100 * rank)
     if name == "cfg5":
         return W.lattice(512, (10, 50), 256, "bf16", 5 + 100 * rank)
+    if name == "cfg5_h512":
+        return W.lattice(512, (10, 50), 512, "bf16", 5 + 100 * rank)
     if name == "cfg5_gru":
         return W.lattice(512, (10, 50), 256, "bf16", 5 + 100 * rank, cell="latticegru")
     if name == "cfg4_treefc":
@@ -298,7 +302,7 @@ def main():
     ap.add_argument("--layout", default="schedule", choices=["schedule", "pq"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--staging", default="auto", choices=["auto", "off"])
-    ap.add_argument("--fsm", default="learned", choices=["learned", "priority"])
+    ap.add_argument("--fsm", default="learned", choices=["learned", "learned_instance", "priority"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -320,13 +324,14 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2302_03851_b200 import edbatch as E
-    from paper_2302_03851_b200.sharding import gather_roots
+    from paper_2302_03851_b200.sharding import RootGather
 
     wl = make_workload(args.config, rank, world, args.scaling)
     layout = E.ED_LAYOUT_PQ if args.layout == "pq" else E.ED_LAYOUT_SCHEDULE_ORDER
     fsm_info = {"fsm": args.fsm}
-    if args.fsm == "learned":  # PAPER §2.3: Q-learned per topology, offline, not timed
-        learned = E.ed_fsm_learn(wl.graphs, wl.types)
+    if args.fsm.startswith("learned"):  # PAPER §2.3: Q-learned per topology, offline, not timed
+        # episodes over the merged minibatch (the graph ed_plan schedules) unless learned_instance
+        learned = E.ed_fsm_learn(wl.graphs, wl.types, merged=args.fsm == "learned")
         fsm = learned.table
         fsm_info.update(fsm_episodes=learned.info["episodes"], fsm_learn_ms=round(learned.info["learn_us"] / 1e3, 3))
     else:
@@ -336,14 +341,19 @@ def main():
     weights = E.DeviceWeights(wl.types, wl.params)
     ws = E.Workspace(plan)
     tdt = torch.bfloat16 if wl.dtype == "bf16" else torch.float32
-    out = torch.zeros(len(wl.graphs), wl.hidden, dtype=tdt, device="cuda")
+    rg = None
+    if dist:  # the sharded path's one collective (root rows all-gathered over NCCL / NVLink), set up once
+        rg = RootGather(wl.shard_idx, wl.n_total, wl.hidden, tdt, "cuda")
+        out = rg.local                          # ed_execute writes the roots straight into the send block
+    else:
+        out = torch.zeros(len(wl.graphs), wl.hidden, dtype=tdt, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 256 MB > L2
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
         E.ed_execute(plan, weights, ws, out)
-        if dist:
-            gather_roots(out, wl.shard_idx, wl.n_total)
+        if rg:
+            rg()
     torch.cuda.synchronize()
 
     clocks = ClockSampler()
@@ -358,15 +368,15 @@ def main():
         flush.zero_()                          # untimed: evict L2 between timed steps
         evs[k][0].record(stream)
         E.ed_execute(plan, weights, ws, out)
-        if dist:  # the sharded path's one collective: root rows all-gathered (NCCL / NVLink)
-            gather_roots(out, wl.shard_idx, wl.n_total)
+        if rg:  # the sharded path's one collective: root rows all-gathered (NCCL / NVLink)
+            rg()
         evs[k][1].record(stream)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     clock_rec = clocks.stop(max(world, 1)) if rank == 0 else None
     times = [a.elapsed_time(b) for a, b in evs]
-    ms_local = sum(times) / len(times)
+    ms_local = statistics.median(times)        # median of the timed runs
     step_ns = ws.step_times_ns()               # in-kernel %globaltimer, last timed execute
     ms = ms_local
     if dist:
@@ -377,7 +387,8 @@ def main():
     value = n_inst_total / (ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers: ed_plan + upload + execute + readback
-    host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    res_shape = (wl.n_total, wl.hidden) if rg else tuple(out.shape)
+    host_out = torch.empty(res_shape, dtype=out.dtype, pin_memory=True)
     e2e_times = []
     h2d = d2h = 0
     for k in range(args.e2e_steps + 2):
@@ -387,17 +398,16 @@ def main():
         p2 = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging)   # host scheduling + layout
         ws.plan_info = p2.info
         E.ed_execute(p2, weights, ws, out)                         # uploads the step table (H2D)
-        if dist:
-            gather_roots(out, wl.shard_idx, wl.n_total)
-        host_out.copy_(out, non_blocking=True)                     # D2H of the step's result
+        res = rg() if rg else out
+        host_out.copy_(res, non_blocking=True)                     # D2H of the step's result
         b.record(stream)
         torch.cuda.synchronize()
         if k >= 2:
             e2e_times.append(a.elapsed_time(b))
-        h2d, d2h = p2.upload_bytes, out.numel() * out.element_size()
+        h2d, d2h = p2.upload_bytes, host_out.numel() * host_out.element_size()
         del p2
     ws.plan_info = plan.info
-    e2e_ms = sum(e2e_times) / len(e2e_times)
+    e2e_ms = statistics.median(e2e_times)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -269,7 +269,9 @@ ed_status_t ed_workspace_release(const void *workspace);
  * eps = max(eps_floor, eps0 * eps_decay^(episode / eps_every)).  Every check_every episodes the
  * greedy table is evaluated with Alg. 1 (A-3 fallback for unseen states) on all instances and
  * training stops when the batch total reaches the App. B.3 lower bound (sum over instances).
- * The result is an FSM table for ed_plan (state -> argmax_a Q) plus the Q values.
+ * The result is an FSM table for ed_plan plus the Q values: pi(S) = argmax_a Q(S, a) over the
+ * actions tried in S, taken from the best greedy table evaluated (the checkpoints and
+ * the final Q; fewest batches, earliest on ties).
  * Host only; deterministic for a given seed; no CUDA call. ------------------------------------ */
 typedef struct {
   int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE                                            */
@@ -277,12 +279,17 @@ typedef struct {
   int32_t max_episodes;  /* paper: 1000                                                   */
   int32_t check_every;   /* paper: 50                                                     */
   int32_t eps_every;     /* episodes per epsilon decay step                                       */
-  int32_t reserved;      /* must be 0                                                             */
+  int32_t episode_graph; /* ED_RL_EPISODE_INSTANCE: one instance graph per episode (cycling);
+                            ED_RL_EPISODE_MERGED: every episode runs Alg. 1 over the merged minibatch
+                            (the dataflow graph ed_plan schedules); checkpoints and the
+                            lower bound are then those of the merged graph                          */
   double alpha;          /* Eq. 1 coefficient, >= 0                                               */
   double lr;             /* learning rate in (0, 1]                                               */
   double eps0, eps_decay, eps_floor;
   uint64_t seed;         /* SplitMix64 seed                                                       */
-} ed_rl_config_t;        /* defaults (A-26): SORT, 4, 1000, 50, 10, 0, .5, .1, .5, .95, .02 */
+} ed_rl_config_t;        /* defaults (A-26): SORT, 4, 1000, 50, 10, INSTANCE, .5, .1, .5, .95, .02 */
+#define ED_RL_EPISODE_INSTANCE 0
+#define ED_RL_EPISODE_MERGED   1
 
 typedef struct ed_fsm_learned_s ed_fsm_learned_t;  /* opaque; owned by the caller */
 

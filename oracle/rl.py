@@ -21,8 +21,15 @@ Readings where the paper is silent (A-26; defaults
   * epsilon-greedy over the ready types (ascending type id): u = (x >> 11) * 2^-53 of one
     SplitMix64 draw; if u < epsilon the action is ready[y % len(ready)] for a second draw y, else
     the greedy argmax (ties to the lowest type id).
-  * the learned FSM table maps every state seen in Q to its greedy action; evaluation runs that
-    table through Alg. 1 with the A-3 fallback key[0] for unseen states (what ed_plan executes).
+  * the learned FSM table maps every state seen in Q to argmax_a Q(S, a) over the actions tried
+    in S ("greedy argmax over ready types with table entries"; ties to the
+    lowest type id); evaluation runs that table through Alg. 1 with the A-3 fallback key[0] for
+    unseen states (what ed_plan executes).
+  * the returned table is the best greedy table evaluated (the checkpoints, then the final Q;
+    fewest batches, earliest on ties): with an early stop, the table that reached the bound.
+  * the training graphs are either the instances (one per episode, cycling) or the one merged
+    minibatch graph -- the dataflow graph Alg. 1 actually runs on ("the environment
+    is the dataflow graph"); the caller passes [Merged(all instances)] for the latter.
 """
 from __future__ import annotations
 
@@ -73,6 +80,7 @@ class RLResult:
     returns: List[float] = field(default_factory=list)                 # per-episode sum of rewards
     batches: List[int] = field(default_factory=list)                   # per-episode batch count
     lower_bound: int = 0
+    final_batches: int = 0                                             # batches of the returned table
 
 
 def ready_types(key: tuple, encoder: str) -> List[int]:
@@ -91,9 +99,13 @@ def greedy(q: Dict[Tuple[tuple, int], float], key: tuple, ready: Sequence[int]) 
 
 
 def policy_table(q: Dict[Tuple[tuple, int], float], encoder: str) -> Dict[tuple, int]:
-    """pi(S) = argmax_a Q(S, a) for every state that has Q entries."""
-    keys = sorted({k for k, _ in q}, key=repr)
-    return {k: greedy(q, k, ready_types(k, encoder)) for k in keys}
+    """pi(S) = argmax_a Q(S, a) for every state that has Q entries, a over the actions with a
+    Q entry in S; ties to the lowest type id."""
+    table = {}
+    for k in sorted({k for k, _ in q}, key=repr):
+        tried = [a for a in ready_types(k, encoder) if (k, a) in q]
+        table[k] = greedy(q, k, tried)
+    return table
 
 
 def reward(m: Merged, executed: Sequence[bool], a: int, alpha: float) -> float:
@@ -148,6 +160,7 @@ def train(graphs: Sequence[Merged], cfg: RLConfig = RLConfig()) -> RLResult:
     q: Dict[Tuple[tuple, int], float] = {}
     lb = sum(lower_bound(m) for m in graphs)
     res = RLResult(q=q, table={}, episodes=0, lower_bound=lb)
+    best = None
     for ep in range(cfg.max_episodes):
         m = graphs[ep % len(graphs)]
         eps = max(cfg.eps_floor, cfg.eps0 * cfg.eps_decay ** (ep // cfg.eps_every))
@@ -160,7 +173,13 @@ def train(graphs: Sequence[Merged], cfg: RLConfig = RLConfig()) -> RLResult:
             table = policy_table(q, cfg.encoder)
             total = sum(len(fsm_schedule(g, table, cfg.encoder)) for g in graphs)
             res.checkpoints.append((ep + 1, total))
+            if best is None or total < best:
+                best, res.table = total, table
             if total == lb:
                 break
-    res.table = policy_table(q, cfg.encoder)
+    table = policy_table(q, cfg.encoder)
+    total = sum(len(fsm_schedule(g, table, cfg.encoder)) for g in graphs)
+    if best is None or total < best:
+        best, res.table = total, table
+    res.final_batches = best
     return res

@@ -641,23 +641,28 @@ ed_status_t ed_fsm_learn(const ed_graph_t *graphs, int32_t num_graphs, const ed_
   tmp.types.assign(types, types + num_types);
   ed_status_t st = validate_and_merge(&tmp, graphs, num_graphs);
   if (st != ED_OK) return st;
-  std::vector<ed::RlGraph> gs(num_graphs);
+  // Episode graphs: each instance with local ids, or (ED_RL_EPISODE_MERGED) the merged minibatch
+  // with its global ids (one graph: the dataflow graph ed_plan schedules).
+  const bool merged = cfg->episode_graph == ED_RL_EPISODE_MERGED;
+  std::vector<ed::RlGraph> gs(merged ? 1 : num_graphs);
   int64_t base = 0;
   for (int gi = 0; gi < num_graphs; ++gi) {
-    ed::RlGraph &g = gs[gi];
-    g.n = graphs[gi].num_nodes;
-    g.type.assign(tmp.gtype.begin() + base, tmp.gtype.begin() + base + g.n);
-    g.pred_off.assign(1, 0);
-    for (int v = 0; v < g.n; ++v) {
+    ed::RlGraph &g = gs[merged ? 0 : gi];
+    const int64_t off = merged ? 0 : base;  // id offset of this graph's first node in g
+    if (g.pred_off.empty()) g.pred_off.assign(1, 0);
+    const int32_t n = graphs[gi].num_nodes;
+    g.type.insert(g.type.end(), tmp.gtype.begin() + base, tmp.gtype.begin() + base + n);
+    for (int v = 0; v < n; ++v) {
       std::vector<int32_t> pr;
       for (int k = tmp.in_off[base + v]; k < tmp.in_off[base + v + 1]; ++k)
-        if (tmp.in_idx[k] >= 0) pr.push_back(static_cast<int32_t>(tmp.in_idx[k] - base));
+        if (tmp.in_idx[k] >= 0) pr.push_back(static_cast<int32_t>(tmp.in_idx[k] - off));
       std::sort(pr.begin(), pr.end());
       pr.erase(std::unique(pr.begin(), pr.end()), pr.end());  // distinct dependencies
       g.preds.insert(g.preds.end(), pr.begin(), pr.end());
       g.pred_off.push_back(static_cast<int32_t>(g.preds.size()));
     }
-    base += g.n;
+    g.n += n;
+    base += n;
   }
   ed_fsm_learned_t *fl = new (std::nothrow) ed_fsm_learned_t();
   if (!fl) return fail(ED_E_OOM, "out of host memory");

@@ -163,10 +163,16 @@ std::vector<int32_t> ascending(const std::vector<int32_t> &key) {
   return r;
 }
 
+// pi(S) = argmax_a Q(S, a) over the actions tried in S ("greedy argmax over
+// ready types with table entries"); ties to the lowest type id.  Unseen pairs are valued 0 only
+// while exploring (greedy() above), never in the exported table.
 std::map<std::vector<int32_t>, int32_t> make_table(const std::map<std::pair<std::vector<int32_t>, int32_t>, double> &q) {
   std::map<std::vector<int32_t>, int32_t> t;
-  for (const auto &kv : q) t.emplace(kv.first.first, 0);
-  for (auto &kv : t) kv.second = greedy(q, kv.first, ascending(kv.first));
+  for (const auto &kv : q) {
+    auto it = t.find(kv.first.first);
+    if (it == t.end()) t.emplace(kv.first.first, kv.first.second);  // actions visited ascending
+    else if (kv.second > q.at({kv.first.first, it->second})) it->second = kv.first.second;
+  }
   return t;
 }
 
@@ -196,7 +202,7 @@ int64_t evaluate(const std::vector<RlGraph> &gs, const std::vector<Prepared> &Ps
 int rl_train(const std::vector<RlGraph> &gs, int nt, const ed_rl_config_t &cfg, RlResult *out) {
   if (gs.empty() || cfg.n_steps < 1 || cfg.max_episodes < 0 || cfg.check_every < 1 || cfg.eps_every < 1 ||
       !(cfg.alpha >= 0.0) || !(cfg.lr > 0.0 && cfg.lr <= 1.0) || (cfg.encoder != ED_ENC_SORT && cfg.encoder != ED_ENC_BASE) ||
-      cfg.reserved != 0)
+      (cfg.episode_graph != ED_RL_EPISODE_INSTANCE && cfg.episode_graph != ED_RL_EPISODE_MERGED))
     return -1;
   std::vector<Prepared> Ps;
   Ps.reserve(gs.size());
@@ -214,6 +220,7 @@ int rl_train(const std::vector<RlGraph> &gs, int nt, const ed_rl_config_t &cfg, 
   std::vector<Step> trace;
   std::vector<int32_t> key, rt;
   out->episodes = 0;
+  int64_t best = -1;
   for (int ep = 0; ep < cfg.max_episodes; ++ep) {
     const size_t gi = static_cast<size_t>(ep) % gs.size();
     const double eps = std::max(cfg.eps_floor, cfg.eps0 * std::pow(cfg.eps_decay, static_cast<double>(ep / cfg.eps_every)));
@@ -253,13 +260,19 @@ int rl_train(const std::vector<RlGraph> &gs, int nt, const ed_rl_config_t &cfg, 
     }
     out->episodes = ep + 1;
     if ((ep + 1) % cfg.check_every == 0) {
-      const int64_t total = evaluate(gs, Ps, nt, cfg.encoder, make_table(q));
+      auto table = make_table(q);
+      const int64_t total = evaluate(gs, Ps, nt, cfg.encoder, table);
       out->checkpoints.emplace_back(ep + 1, total);
+      if (best < 0 || total < best) { best = total; out->table = std::move(table); }
       if (total == out->lower_bound) break;
     }
   }
-  out->table = make_table(q);
-  out->final_batches = evaluate(gs, Ps, nt, cfg.encoder, out->table);
+  // The returned policy is the best greedy table evaluated (checkpoints, then the final Q);
+  // ties keep the earlier one.  With an early stop it is the table that reached the bound.
+  auto table = make_table(q);
+  const int64_t total = evaluate(gs, Ps, nt, cfg.encoder, table);
+  if (best < 0 || total < best) { best = total; out->table = std::move(table); }
+  out->final_batches = best;
   return 0;
 }
 

@@ -20,6 +20,7 @@ ED_OK = 0
 ED_ZERO_INPUT = -(2 ** 31)
 ED_FP32, ED_BF16 = 0, 1
 ED_ENC_SORT, ED_ENC_BASE = 0, 1
+ED_RL_EPISODE_INSTANCE, ED_RL_EPISODE_MERGED = 0, 1
 ED_LAYOUT_SCHEDULE_ORDER, ED_LAYOUT_PQ = 0, 1
 ED_STAGING_AUTO, ED_STAGING_OFF = 0, 1
 STATUS = {0: "ED_OK", -1: "ED_E_INVALID_ARG", -2: "ED_E_CYCLE", -3: "ED_E_DANGLING", -4: "ED_E_DUP_ID",
@@ -85,7 +86,7 @@ class ed_io_t(ctypes.Structure):
 
 class ed_rl_config_t(ctypes.Structure):
     _fields_ = [("encoder", ctypes.c_int32), ("n_steps", ctypes.c_int32), ("max_episodes", ctypes.c_int32),
-                ("check_every", ctypes.c_int32), ("eps_every", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("check_every", ctypes.c_int32), ("eps_every", ctypes.c_int32), ("episode_graph", ctypes.c_int32),
                 ("alpha", ctypes.c_double), ("lr", ctypes.c_double), ("eps0", ctypes.c_double),
                 ("eps_decay", ctypes.c_double), ("eps_floor", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
@@ -246,12 +247,15 @@ class LearnedFsm:
 
 def ed_fsm_learn(graphs, types, encoder: int = ED_ENC_SORT, alpha: float = 0.5, lr: float = 0.1, eps0: float = 0.5,
                  eps_decay: float = 0.95, eps_every: int = 10, eps_floor: float = 0.02, n_steps: int = 4,
-                 max_episodes: int = 1000, check_every: int = 50, seed: int = 4000) -> LearnedFsm:
-    """Learn an FSM table by tabular N-step Q-learning (include/ed_batch.h ed_fsm_learn)."""
+                 max_episodes: int = 1000, check_every: int = 50, seed: int = 4000,
+                 merged: bool = False) -> LearnedFsm:
+    """Learn an FSM table by tabular N-step Q-learning (include/ed_batch.h ed_fsm_learn).  merged=True
+    runs every episode over the merged minibatch (ED_RL_EPISODE_MERGED) instead of one instance."""
     keep = []
     garr = _graph_arrays(graphs, keep)
     tarr = _type_array(types)
-    cfg = ed_rl_config_t(encoder, n_steps, max_episodes, check_every, eps_every, 0, alpha, lr, eps0, eps_decay,
+    cfg = ed_rl_config_t(encoder, n_steps, max_episodes, check_every, eps_every,
+                         ED_RL_EPISODE_MERGED if merged else ED_RL_EPISODE_INSTANCE, alpha, lr, eps0, eps_decay,
                          eps_floor, seed)
     h = ctypes.c_void_p()
     _check(LIB.ed_fsm_learn(garr, len(graphs), tarr, len(types), ctypes.byref(cfg), ctypes.byref(h)))

@@ -30,36 +30,57 @@ def shard_graphs(graphs, rank: int, world: int):
     return idx, [graphs[i] for i in idx]
 
 
-def gather_roots(out_local, idx: Sequence[int], n_total: int, group=None):
-    """All ranks' root outputs in global instance order (one all-gather of the root
-    rows over NCCL / NVLink).  out_local: [len(idx), h] this rank's roots (instance order of idx).
-    Every rank contributes a padded [max_shard, h] block plus its instance indices; the result is
-    [n_total, h] on every rank.  The only collective of the sharded path (instances are independent,
-    P:73)."""
-    import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    n_local = torch.tensor([len(idx)], device=out_local.device)
-    sizes = [torch.zeros_like(n_local) for _ in range(world)]
-    dist.all_gather(sizes, n_local, group=group)
-    cap = int(max(int(s.item()) for s in sizes))
-    h = out_local.shape[1]
-    pad = torch.zeros(cap, h, dtype=out_local.dtype, device=out_local.device)
-    pad[:len(idx)] = out_local
-    ids = torch.full((cap,), -1, dtype=torch.int64, device=out_local.device)
-    ids[:len(idx)] = torch.as_tensor(list(idx), dtype=torch.int64, device=out_local.device)
-    if dist.get_backend(group) == "nccl":
-        rows = torch.empty(world * cap, h, dtype=out_local.dtype, device=out_local.device)
-        all_ids = torch.empty(world * cap, dtype=torch.int64, device=out_local.device)
-        dist.all_gather_into_tensor(rows, pad, group=group)
-        dist.all_gather_into_tensor(all_ids, ids, group=group)
-    else:
-        rl = [torch.empty_like(pad) for _ in range(world)]
-        il = [torch.empty_like(ids) for _ in range(world)]
-        dist.all_gather(rl, pad, group=group)
+class RootGather:
+    """The root all-gather of the sharded path, set up once per plan.
+
+    Construction (outside any timed region) exchanges the shard sizes and instance ids once and
+    builds a padded [cap, h] send block and a static index map.  ed_execute writes this rank's roots
+    straight into ``local`` (a contiguous view of the send block), so a step is exactly one
+    all_gather_into_tensor of the padded blocks plus one index_select into global instance order:
+    no host sync, no size exchange, no H2D (sizes are static per plan)."""
+
+    def __init__(self, idx: Sequence[int], n_total: int, h: int, dtype, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        dev = torch.device(device)
+        cdev = dev if self.nccl else torch.device("cpu")
+        n_local = torch.tensor([len(idx)], dtype=torch.int64, device=cdev)
+        sizes = [torch.zeros_like(n_local) for _ in range(self.world)]
+        dist.all_gather(sizes, n_local, group=group)
+        self.cap = cap = max(1, int(max(int(s.item()) for s in sizes)))
+        ids = torch.full((cap,), -1, dtype=torch.int64, device=cdev)
+        ids[:len(idx)] = torch.as_tensor(list(idx), dtype=torch.int64)
+        il = [torch.empty_like(ids) for _ in range(self.world)]
         dist.all_gather(il, ids, group=group)
-        rows, all_ids = torch.cat(rl), torch.cat(il)
-    out = torch.empty(n_total, h, dtype=out_local.dtype, device=out_local.device)
-    keep = all_ids >= 0
-    out[all_ids[keep]] = rows[keep]
-    return out
+        all_ids = torch.cat(il).cpu()
+        src = torch.full((n_total,), -1, dtype=torch.int64)
+        pos = torch.nonzero(all_ids >= 0).flatten()
+        src[all_ids[pos]] = pos
+        if bool((src < 0).any()):
+            raise ValueError("RootGather: the shards do not cover every instance")
+        self.src = src.to(dev)
+        self.send = torch.zeros(cap, h, dtype=dtype, device=dev)
+        self.local = self.send[:len(idx)]
+        self.rows = torch.empty(self.world * cap, h, dtype=dtype, device=dev)
+
+    def __call__(self):
+        """[n_total, h] roots of every rank in global instance order."""
+        import torch
+        import torch.distributed as dist
+        if self.nccl:
+            dist.all_gather_into_tensor(self.rows, self.send, group=self.group)
+        else:
+            rl = list(torch.chunk(self.rows, self.world))
+            dist.all_gather(rl, self.send, group=self.group)
+        return self.rows.index_select(0, self.src)
+
+
+def gather_roots(out_local, idx: Sequence[int], n_total: int, group=None):
+    """All ranks' root outputs in global instance order (one-off convenience wrapper over
+    RootGather; a timed loop builds the RootGather once and reuses it)."""
+    rg = RootGather(idx, n_total, out_local.shape[1], out_local.dtype, out_local.device, group)
+    rg.local.copy_(out_local)
+    return rg()

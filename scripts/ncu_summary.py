@@ -11,7 +11,12 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_bytes.sum", "l1tex__t_bytes.sum", "sm__cycles_elapsed.avg.per_second",
         "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
         "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active"]
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+        "lts__t_sectors.sum", "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
+        "lts__t_sectors_srcunit_ltcfabric.sum", "lts__t_sectors_lookup_hit.sum", "lts__t_sectors_lookup_miss.sum",
+        "lts__t_requests_srcunit_tex_op_read.sum", "lts__t_requests_srcunit_tex_op_write.sum",
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 d = {}
 for k in want:
     for i, h in enumerate(hdr):
@@ -40,14 +45,24 @@ tot = sum(v for _, v in ls)
 agg = {}
 for k, v in ls:
     agg.setdefault(k, []).append(v)
-summary = {"report": rep, "metrics": d, "dram_bytes_per_launch": dram,
+l2 = num("lts__t_sectors.sum")
+l2r = num("lts__t_sectors_srcunit_tex_op_read.sum")
+l2w = num("lts__t_sectors_srcunit_tex_op_write.sum")
+alg = float(sys.argv[4]) if len(sys.argv) > 4 else None
+l2info = {"l2_bytes_per_launch": None if l2 is None else l2 * 32, "l2_read_bytes": None if l2r is None else l2r * 32,
+          "l2_write_bytes": None if l2w is None else l2w * 32, "algorithmic_bytes": alg,
+          "l2_over_algorithmic": None if (l2 is None or not alg) else l2 * 32 / alg}
+summary = {"report": rep, "metrics": d, "dram_bytes_per_launch": dram, "l2": l2info,
            "launch_list": {k: {"launches": len(v), "avg_ns": sum(v) / len(v), "share": sum(v) / tot} for k, v in agg.items()}}
 json.dump(summary, open(out_prefix + ".json", "w"), indent=1)
 with open(out_prefix + ".md", "w") as f:
     f.write(f"# ncu summary: {rep}\n\n| metric | value | unit |\n|---|---|---|\n")
     for k, v in d.items():
         f.write(f"| {k} | {v['value']} | {v['unit']} |\n")
-    f.write(f"| dram bytes per launch (read+write) | {dram} | byte |\n\n")
+    f.write(f"| dram bytes per launch (read+write) | {dram} | byte |\n")
+    for k, v in l2info.items():
+        f.write(f"| {k} | {v} | |\n")
+    f.write("\n")
     f.write("## launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold, serialised)\n\n")
     f.write("| kernel | launches | avg us | share of listed time |\n|---|---|---|---|\n")
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):

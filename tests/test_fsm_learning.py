@@ -199,3 +199,54 @@ def test_two_internal_types_learned_beats_priority_and_heuristics():
     agenda = sum(len(run_alg1(m, agenda_chooser(m))) for m in ms)
     assert r.lower_bound <= learned <= min(prio, depth, agenda)
     assert learned < prio
+
+
+# ------------------------------------------------------------------------------------------------
+# episodes over the merged minibatch (the dataflow graph ed_plan schedules)
+# ------------------------------------------------------------------------------------------------
+
+def _all_sort_tables(nt):
+    """Every E_sort FSM table over nt types: one action per ordered key, chosen from the key."""
+    keys = [k for r in range(1, nt + 1) for s in itertools.combinations(range(nt), r)
+            for k in itertools.permutations(s)]
+    for acts in itertools.product(*keys):
+        yield dict(zip(keys, acts))
+
+
+def test_merged_learning_matches_best_enumerated_table_on_lattice_minibatch():
+    """Brute force over policies (SURVEY A-8): on a merged lattice minibatch the table learned with
+    merged episodes executes as few batches as the best of all 4 E_sort tables; per-instance
+    training does not see the cross-instance frontier and may not."""
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.lattice(96, (10, 50), 32, "fp32")
+    got = E.ed_fsm_learn(wl.graphs, wl.types, merged=True)
+    learned = E.ed_plan(wl.graphs, wl.types, got.table).info["num_batches"]
+    best = min(E.ed_plan(wl.graphs, wl.types, list(t.items())).info["num_batches"] for t in _all_sort_tables(2))
+    assert learned == best == got.info["final_batches"]
+    assert got.info["lower_bound"] <= learned
+
+
+@pytest.mark.parametrize("family", ["lattice", "trees"])
+def test_c_learner_merged_bit_exact_with_oracle(family):
+    from paper_2302_03851_b200 import edbatch as E
+    wl = W.lattice(10, (6, 14), 32, "fp32") if family == "lattice" else trees()
+    cfg = RLConfig(max_episodes=150, check_every=50)
+    ref = train([Merged(wl.graphs, len(wl.types))], cfg)
+    got = E.ed_fsm_learn(wl.graphs, wl.types, max_episodes=cfg.max_episodes, check_every=cfg.check_every,
+                         merged=True)
+    assert got.checkpoints == ref.checkpoints
+    assert got.info["lower_bound"] == ref.lower_bound
+    assert got.info["final_batches"] == ref.final_batches
+    assert dict(got.table) == ref.table
+    assert got.q == ref.q
+
+
+def test_exported_policy_ignores_untried_actions():
+    """pi(S) is the argmax over the actions with a Q entry in S; an untried action (0 by
+    the exploration default) must not beat a tried one with a negative value."""
+    q = {((0, 1), 1): -2.0}
+    assert policy_table(q, "sort") == {(0, 1): 1}
+    q[((0, 1), 0)] = -3.0
+    assert policy_table(q, "sort") == {(0, 1): 1}
+    q[((0, 1), 0)] = -1.0
+    assert policy_table(q, "sort") == {(0, 1): 0}

@@ -43,6 +43,14 @@ def _worker(rank, world, port, q):
         local = torch.stack([torch.full((4,), float(i)) for i in idx]) if idx else torch.zeros(0, 4)
         full = gather_roots(local, idx, len(wl.graphs))
         assert torch.equal(full[:, 0], torch.arange(len(wl.graphs), dtype=torch.float32))
+        # bench.py's timed loop: the gather is set up once per plan, the roots are written into its
+        # send block and every step is one all-gather (no size exchange, no host sync)
+        from paper_2302_03851_b200.sharding import RootGather
+        rg = RootGather(idx, len(wl.graphs), 4, torch.float32, "cpu")
+        for step in range(3):
+            rg.local.copy_(torch.stack([torch.full((4,), float(i + 100 * step)) for i in idx]))
+            full = rg()
+            assert torch.equal(full[:, 3], torch.arange(len(wl.graphs), dtype=torch.float32) + 100 * step)
         if rank == 0:
             q.put((t.tolist(), float(ms.item()), shards, wl.num_nodes, len(wl.graphs)))
     finally:
