@@ -158,6 +158,10 @@ struct ed_plan_s {
   bool staging = true;      // bf16: stage gathered cell operands into contiguous blocks
   int64_t op_rows = 0;      // staged operand rows appended to H (rows V+1 ..)
   int32_t ext_root_off = 0, num_ext_roots = 0;  // instances whose output is an input lookup
+  // largest id read from each weight set's emb / emb2 table (-1: none); ed_execute checks them
+  // against emb_rows / emb2_rows, so a bad token fails the call instead of reading out of bounds
+  int32_t max_emb[ed::kMaxWeightSets], max_emb2[ed::kMaxWeightSets];
+  std::string bad_ext;  // non-empty: an external input where the kernel cannot read one
   int64_t staged = 0, staged_bytes = 0;
   int64_t dst_base = 0;     // idx offset of dst_off[V + 2] (then the copy destinations)
   double plan_us = 0, sched_us = 0, layout_us = 0, validate_us = 0, lower_us = 0;
@@ -172,6 +176,8 @@ struct ed_plan_s {
 // ------------------------------------------------------------------------------------------------
 static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, int32_t ng) {
   const int nt = static_cast<int>(pl->types.size());
+  std::fill(pl->max_emb, pl->max_emb + ed::kMaxWeightSets, -1);
+  std::fill(pl->max_emb2, pl->max_emb2 + ed::kMaxWeightSets, -1);
   int64_t total = 0;
   for (int gi = 0; gi < ng; ++gi) {
     const ed_graph_t &g = graphs[gi];
@@ -210,6 +216,25 @@ static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, i
           if (x == v) return fail(ED_E_CYCLE, tag + ": self loop at node " + std::to_string(v));
           pl->in_idx.push_back(static_cast<int32_t>(base + x));
         } else {
+          if (x != ED_ZERO_INPUT) {
+            // external (-1 - id): a word row of the op's weight set (TreeFC / MV-RNN children,
+            // SURVEY A-6) or the end char x_e of a lattice word (slot 1, read from emb2); any other
+            // slot has no table to read it from
+            const int j = k - g.in_off[v];
+            const bool to_emb = ot.cell_kind == ED_CELL_TREEFC_INTERNAL || ot.cell_kind == ED_CELL_MVRNN_INTERNAL;
+            const bool to_emb2 = ot.cell_kind == ED_CELL_LATTICE_WORD && j == 1;
+            if (j >= ot.num_slots || !(to_emb || to_emb2)) {
+              // a legal dataflow graph for the scheduler, but the kernel has no row to read:
+              // planning proceeds, ed_execute refuses the plan
+              if (pl->bad_ext.empty())
+                pl->bad_ext = tag + ": node " + std::to_string(v) + " slot " + std::to_string(j) +
+                              " takes an external input, which this cell cannot read (only TreeFC / MV-RNN"
+                              " children and a lattice word's end char are table rows)";
+            } else {
+              int32_t &mx = to_emb ? pl->max_emb[ot.weight_set] : pl->max_emb2[ot.weight_set];
+              mx = std::max(mx, -1 - x);
+            }
+          }
           pl->in_idx.push_back(x);  // ED_ZERO_INPUT or external (-1 - id)
         }
       }
@@ -219,11 +244,16 @@ static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, i
         if (!g.ext) return fail(ED_E_INVALID_ARG, tag + ": type with ext but ext == NULL");
         if (g.ext[v] < 0) return fail(ED_E_INVALID_ARG, tag + ": node " + std::to_string(v) + " has no ext token");
         pl->ext[base + v] = g.ext[v];
+        pl->max_emb[ot.weight_set] = std::max(pl->max_emb[ot.weight_set], g.ext[v]);
       }
     }
     if (g.root >= n) return fail(ED_E_DANGLING, tag + ": root out of range");
     if (g.root < 0 && n > 0) return fail(ED_E_DANGLING, tag + ": external root on a graph with ops");
     pl->roots[gi] = g.root >= 0 ? static_cast<int32_t>(base + g.root) : g.root;
+    if (g.root < 0) {  // a 0-op instance: its output is the input row (-1 - root) of types[0]'s table
+      int32_t &mx = pl->max_emb[pl->types[0].weight_set];
+      mx = std::max(mx, -1 - g.root);
+    }
     base += n;
   }
   // acyclicity (Kahn); the consumers CSR and in-degrees are kept for Alg. 1
@@ -918,6 +948,30 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   if (w->num_sets <= 0 || w->num_sets > ed::kMaxWeightSets || !w->sets) return fail(ED_E_INVALID_ARG, "bad weights");
   for (const auto &ot : pl->types)
     if (ot.weight_set >= w->num_sets) return fail(ED_E_INVALID_ARG, "weight set missing");
+  if (!pl->bad_ext.empty()) return fail(ED_E_UNSUPPORTED, pl->bad_ext);
+  for (const auto &ot : pl->types) {
+    const ed_weight_set_t &s_ = w->sets[ot.weight_set];
+    const std::string tag = "weight set " + std::to_string(ot.weight_set);
+    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL && (!s_.mat || s_.emb_rows <= 0 || !s_.emb || !s_.W || !s_.b || !s_.W2))
+      return fail(ED_E_INVALID_ARG, "MV-RNN weight set needs W, b, W2 (W_M), emb and mat with emb_rows > 0");
+    if (!s_.W || !s_.b) return fail(ED_E_INVALID_ARG, tag + ": W and b must be non-null");
+    if ((ot.cell_kind == ED_CELL_TAGGER || ot.cell_kind == ED_CELL_LATTICE_WORD) && (!s_.W2 || !s_.b2))
+      return fail(ED_E_INVALID_ARG, tag + ": this cell needs W2 and b2");
+  }
+  for (int k = 0; k < ed::kMaxWeightSets; ++k) {  // every table id the plan reads is in range
+    const bool used1 = pl->max_emb[k] >= 0, used2 = pl->max_emb2[k] >= 0;
+    if (!used1 && !used2) continue;
+    if (k >= w->num_sets) return fail(ED_E_INVALID_ARG, "weights: missing weight set " + std::to_string(k));
+    const ed_weight_set_t &s_ = w->sets[k];
+    if (used1 && (!s_.emb || pl->max_emb[k] >= s_.emb_rows))
+      return fail(ED_E_INVALID_ARG, "weight set " + std::to_string(k) + ": token / external id " +
+                                        std::to_string(pl->max_emb[k]) + " needs emb with more than that many rows (emb_rows " +
+                                        std::to_string(s_.emb_rows) + ")");
+    if (used2 && (!s_.emb2 || pl->max_emb2[k] >= s_.emb2_rows))
+      return fail(ED_E_INVALID_ARG, "weight set " + std::to_string(k) + ": external char id " +
+                                        std::to_string(pl->max_emb2[k]) + " needs emb2 with more than that many rows (emb2_rows " +
+                                        std::to_string(s_.emb2_rows) + ")");
+  }
   int sms = 0, major = 0, minor = 0;
   int e = ed::device_check(&sms, &major, &minor);
   if (e) return fail(ED_E_CUDA, std::string("cuda: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -1001,11 +1055,6 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   for (int k = 0; k < w->num_sets; ++k) {
     const ed_weight_set_t &ws_ = w->sets[k];
     p.w[k] = ed::DevWeightSet{ws_.W, ws_.b, ws_.W2, ws_.b2, ws_.emb, ws_.emb2, ws_.mat, ws_.emb_rows, ws_.emb2_rows};
-  }
-  for (const auto &ot : pl->types) {
-    const ed_weight_set_t &s_ = w->sets[ot.weight_set];
-    if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL && (!s_.mat || s_.emb_rows <= 0 || !s_.emb || !s_.W || !s_.b || !s_.W2))
-      return fail(ED_E_INVALID_ARG, "MV-RNN weight set needs W, b, W2 (W_M), emb and mat with emb_rows > 0");
   }
   if (pl->dtype == ED_BF16) {
     const int64_t hh = pl->hidden;

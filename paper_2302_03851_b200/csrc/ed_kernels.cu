@@ -47,6 +47,16 @@ constexpr int kBiasBytes = 5 * 512 * 4;           // G * h fp32 (G * h <= 2560)
 constexpr int kWoutBytes = 12 * 1024;             // output-linear weights [C][h] fp32 (else read from L2)
 constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes + kWoutBytes + 256;
 constexpr int kEpiThreads = 128;
+// setmaxnreg budgets (multiples of 8): 128 x kEpiRegs + 256 x kProdRegs <= 64K registers per SM
+#ifndef ED_EPI_REGS
+#define ED_EPI_REGS 232
+#endif
+#ifndef ED_PROD_REGS
+#define ED_PROD_REGS 136
+#endif
+constexpr int kEpiRegs = ED_EPI_REGS;
+constexpr int kProdRegs = ED_PROD_REGS;
+static_assert(kEpiThreads * kEpiRegs + (kThreadsTC - kEpiThreads) * kProdRegs <= 65536, "register budget");
 
 
 // ------------------------------------------------------------------------------------------------
@@ -133,6 +143,11 @@ __device__ __forceinline__ const void *lds_ptr(const void *const *p) {
   unsigned long long v;
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)));
   return reinterpret_cast<const void *>(v);
+}
+__device__ __forceinline__ float4 lds_f4(const float *p) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(p)));
+  return v;
 }
 __device__ __forceinline__ void sts_ptr(const void **p, const void *v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(reinterpret_cast<unsigned long long>(v)) : "memory");
@@ -245,6 +260,13 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
 __device__ __forceinline__ int ready_since_launch(const KParams &p, int e, int tgt) {
   return static_cast<int>(static_cast<uint32_t>(ld_acquire_s32(p.ready + e)) - (p.seq - 1u) * static_cast<uint32_t>(tgt));
 }
+// Watchdog: report the stuck dependency, then abort the launch.  Out of line, so the printf
+// argument marshalling does not cost registers in every polling loop.
+__device__ __noinline__ void watchdog_abort(int cell, int out_row0, int row, int ready, int need) {
+  printf("ed_batch watchdog: block %d thread %d cell %d out_row0 %d row %d ready %d need %d\n", blockIdx.x,
+         threadIdx.x, cell, out_row0, row, ready, need);
+  __trap();
+}
 __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep &st) {
   if (e < 0 || e >= p.rows) return;  // external rows are static
   const int tgt = __ldg(p.target + e);
@@ -338,8 +360,14 @@ template <> __device__ __forceinline__ float act_tanh<float>(float x) { return t
 template <typename T> __device__ __forceinline__ float act_exp(float x) { return __expf(x); }
 template <> __device__ __forceinline__ float act_exp<float>(float x) { return expf(x); }
 
+// Slot j (0 or 1) of a step: selects instead of st.mode[j] / st.arg[j], so the step record stays in
+// registers (a runtime index would put it in local memory, and with 224 KB of shared memory per
+// CTA the L1 left for local memory is small: local loads go to L2).
+__device__ __forceinline__ int slot_mode(const DevStep &st, int j) { return j == 0 ? st.mode[0] : st.mode[1]; }
+__device__ __forceinline__ int slot_arg(const DevStep &st, int j) { return j == 0 ? st.arg[0] : st.arg[1]; }
 __device__ __forceinline__ int slot_entry(const DevStep &st, const int32_t *idx, int j, int i) {
-  return st.mode[j] == 1 ? st.arg[j] + i : __ldg(idx + st.arg[j] + i);
+  const int mode = slot_mode(st, j), arg = slot_arg(st, j);
+  return mode == 1 ? arg + i : __ldg(idx + arg + i);
 }
 
 template <typename T>
@@ -417,12 +445,13 @@ __device__ __forceinline__ bool segment_contig(const KParams &p, const DevStep &
     if (s == 0) return false;
     slot = 0;
   }
-  if (st.mode[slot] == 2) {  // staged block (rows written by the producers' epilogues)
-    *base = __ldg(p.idx + st.arg[slot] + st.m);
+  const int mode = slot_mode(st, slot), arg = slot_arg(st, slot);
+  if (mode == 2) {  // staged block (rows written by the producers' epilogues)
+    *base = __ldg(p.idx + arg + st.m);
     return true;
   }
-  *base = st.arg[slot];
-  return st.mode[slot] == 1;
+  *base = arg;
+  return mode == 1;
 }
 
 __device__ __forceinline__ float c_of(const KParams &p, int e, int j) {
@@ -912,7 +941,7 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4 &v, float *out) {
 template <int CELL>
 __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
                                               uint32_t parity, int row_tile, int col_tile, int r,
-                                              const float *sbias, unsigned long long *tr = nullptr) {
+                                              const float *sbias, bool bias_smem, unsigned long long *tr = nullptr) {
   using CC = CellCfg<CELL>;
   constexpr int G = CC::G, NC = CC::NC, NH = CC::NH;
   const int h = p.hidden;
@@ -933,11 +962,12 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   const float4 *cp1 = reinterpret_cast<const float4 *>(p.C + static_cast<size_t>(e1) * h + jb);
   const __nv_bfloat16 *Hb = static_cast<const __nv_bfloat16 *>(p.H);
   int dbeg = 0, dend = 0;  // copies of this result row (staged operand rows, instance output)
-  __nv_bfloat16 *cpy0 = nullptr;  // the first copy's row, resolved up front
+  __nv_bfloat16 *cpy0 = nullptr, *cpy1 = nullptr;  // the first two copies' rows, resolved up front
   if (valid && CELL != kCellLatticeLink) {
     dbeg = __ldg(p.dst_off + st.out_row0 + i);
     dend = __ldg(p.dst_off + st.out_row0 + i + 1);
     if (dbeg < dend) cpy0 = copy_row<__nv_bfloat16>(p, __ldg(p.idx + dbeg++));
+    if (dbeg < dend) cpy1 = copy_row<__nv_bfloat16>(p, __ldg(p.idx + dbeg++));
   }
   const uint4 *hp0 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e0) * h + jb);
   const uint4 *hp1 = reinterpret_cast<const uint4 *>(Hb + static_cast<size_t>(e1) * h + jb);
@@ -950,43 +980,64 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       for (int w = wbeg; w < wend; ++w) wait_row(p, __ldg(p.idx + w), st);  // words ending here (c^w, l_w)
     }
   }
-  float4 cn[NC > 0 ? 2 * NC : 1];
-  uint4 hn[NH > 0 ? NH : 1];
+  // Child / previous-state rows are prefetched two 8-unit passes ahead (passes are processed in
+  // pairs, each with its own register buffer): both passes of a 16-unit tile are loaded before the
+  // accumulator wait, so the tail steps' epilogue has no L2 round trip inside the pass loop.
+  const int nsteps = ngroups * 2;  // even
+  float4 cbuf[2][NC > 0 ? 2 * NC : 1];
+  uint4 hbuf[2][NH > 0 ? NH : 1];
 #pragma unroll
-  for (int q = 0; q < 2 * NC; ++q) cn[q] = __ldcg((q < 2 ? cp0 : cp1) + (q & 1));
+  for (int b2 = 0; b2 < 2; ++b2) {
 #pragma unroll
-  for (int q = 0; q < NH; ++q) hn[q] = __ldcg(q == 0 ? hp0 : hp1);
+    for (int q = 0; q < 2 * NC; ++q) cbuf[b2][q] = __ldcg((q < 2 ? cp0 : cp1) + b2 * 2 + (q & 1));
+#pragma unroll
+    for (int q = 0; q < NH; ++q) hbuf[b2][q] = __ldcg((q == 0 ? hp0 : hp1) + b2);
+  }
   mbar_wait(tfull_bar, parity);
   tc_fence_after();
   if (tr != nullptr && r == 0) *tr = globaltimer();
   __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
   const size_t orow = static_cast<size_t>(st.out_row0 + (valid ? i : 0));
-  const int nsteps = ngroups * 2;
+  // A warp whose 32 rows all lie past m skips the pass loop: tcgen05.ld bandwidth (~64 B/clk per
+  // SM) is shared by the four epilogue warps, so small-m tail tiles read TMEM for their live rows only.
+  const bool warp_live = row_tile * kTileM + (r & ~31) < st.m;
 #pragma unroll 1
-  for (int sp = 0; sp < nsteps; ++sp) {
+  for (int sp0 = 0; sp0 < (warp_live ? nsteps : 0); sp0 += 2) {
+#pragma unroll
+  for (int b2 = 0; b2 < 2; ++b2) {
+    const int sp = sp0 + b2;
     const int gq = sp >> 1, half = sp & 1;
     float4 cc[NC > 0 ? 2 * NC : 1];
     uint4 hc[NH > 0 ? NH : 1];
 #pragma unroll
-    for (int q = 0; q < 2 * NC; ++q) cc[q] = cn[q];
+    for (int q = 0; q < 2 * NC; ++q) cc[q] = cbuf[b2][q];
 #pragma unroll
-    for (int q = 0; q < NH; ++q) hc[q] = hn[q];
-    if (sp + 1 < nsteps) {
+    for (int q = 0; q < NH; ++q) hc[q] = hbuf[b2][q];
+    if (sp + 2 < nsteps) {
 #pragma unroll
-      for (int q = 0; q < 2 * NC; ++q) cn[q] = __ldcg((q < 2 ? cp0 : cp1) + (sp + 1) * 2 + (q & 1));
+      for (int q = 0; q < 2 * NC; ++q) cbuf[b2][q] = __ldcg((q < 2 ? cp0 : cp1) + (sp + 2) * 2 + (q & 1));
 #pragma unroll
-      for (int q = 0; q < NH; ++q) hn[q] = __ldcg((q == 0 ? hp0 : hp1) + (sp + 1));
+      for (int q = 0; q < NH; ++q) hbuf[b2][q] = __ldcg((q == 0 ? hp0 : hp1) + (sp + 2));
     }
     float z[G][8];
 #pragma unroll
     for (int g = 0; g < G; ++g) tmem_ld8(tacc + static_cast<uint32_t>(gq * G * 16 + g * 16 + half * 8), z[g]);
     tmem_wait_ld();
+    if (tr != nullptr && r == 0 && sp < 2) tr[4 + 2 * sp] = globaltimer();
     if (!valid) continue;
     const int j0 = jb + sp * 8;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float4 b0 = *reinterpret_cast<const float4 *>(sbias + g * h + j0);
-      const float4 b1 = *reinterpret_cast<const float4 *>(sbias + g * h + j0 + 4);
+      // explicit state spaces: a generic load of the shared bias would be ordered behind this
+      // thread's outstanding global stores of the previous pass (an L2 round trip per pass)
+      float4 b0, b1;
+      if (bias_smem) {
+        b0 = lds_f4(sbias + g * h + j0);
+        b1 = lds_f4(sbias + g * h + j0 + 4);
+      } else {
+        b0 = __ldg(reinterpret_cast<const float4 *>(sbias + g * h + j0));
+        b1 = __ldg(reinterpret_cast<const float4 *>(sbias + g * h + j0 + 4));
+      }
       z[g][0] += b0.x; z[g][1] += b0.y; z[g][2] += b0.z; z[g][3] += b0.w;
       z[g][4] += b1.x; z[g][5] += b1.y; z[g][6] += b1.z; z[g][7] += b1.w;
     }
@@ -1089,6 +1140,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       const uint4 hv4 = make_uint4(packed[0], packed[1], packed[2], packed[3]);
       *reinterpret_cast<uint4 *>(H + orow * h + j0) = hv4;
       if (cpy0 != nullptr) *reinterpret_cast<uint4 *>(cpy0 + j0) = hv4;
+      if (cpy1 != nullptr) *reinterpret_cast<uint4 *>(cpy1 + j0) = hv4;
       for (int d = dbeg; d < dend; ++d) {
         __nv_bfloat16 *dst = copy_row<__nv_bfloat16>(p, __ldg(p.idx + d));
         if (dst != nullptr) *reinterpret_cast<uint4 *>(dst + j0) = hv4;
@@ -1100,10 +1152,15 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
       cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
     }
+    if (tr != nullptr && r == 0 && sp < 2) tr[5 + 2 * sp] = globaltimer();
   }
+  }
+  if (tr != nullptr && r == 0) tr[1] = globaltimer();
   if (valid) {
     asm volatile("fence.proxy.async.global;" ::: "memory");  // rows may be read by TMA (async proxy)
+    if (tr != nullptr && r == 0) tr[2] = globaltimer();
     publish_row(p, static_cast<int>(orow), ngroups * 16);
+    if (tr != nullptr && r == 0) tr[3] = globaltimer();
   }
 }
 
@@ -1239,7 +1296,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   uint32_t tab_tile = 0;    // loader threads: row-table buffer toggle
   uint32_t off = 0;         // running item offset (work rotation)
 
-  // Every warp role walks the steps in order; there is no grid barrier between steps (dataflow).
+  // Register split per warpgroup (setmaxnreg): the epilogue warpgroup (warps 0-3) keeps the gate
+  // math, its prefetched child rows and copy pointers in registers; the MMA issuer, the weight
+  // loader and the operand loaders (warps 4-11) need few.  Every role walks the steps in order;
+  // there is no grid barrier between steps (dataflow).
+  if (warp < 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
   for (int s = 0; s < p.num_steps; ++s) {
     const DevStep st = p.steps[s];
     const int T = step_items(st, h);
@@ -1279,7 +1341,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const int kps = step_kps(st, kc_total, &abytes);
     const uint32_t boff = kps > 1 ? kps * abytes : static_cast<uint32_t>(kAStage);  // B region of a stage
     const uint32_t bchunk = static_cast<uint32_t>(ncols) * 128u;
-    if (warp < 4) {
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
       const bool bias_smem = bsrc != nullptr && st.cell != ED_CELL_LINEAR_OUT && st.gates * h * 4 <= kBiasBytes;
@@ -1298,35 +1359,35 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         const uint32_t par = (pipe.ti >> 1) & 1u;
         switch (st.cell) {
           case ED_CELL_TREELSTM_LEAF:
-            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREELSTM_INTERNAL:
-            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEGRU_LEAF:
-            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEGRU_INTERNAL:
-            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEFC_INTERNAL:
-            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LSTM:
-            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_CHAR:
-            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICEGRU_CHAR:
-            umma_epilogue<ED_CELL_LATTICEGRU_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICEGRU_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICEGRU_WORD:
-            umma_epilogue<ED_CELL_LATTICEGRU_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICEGRU_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_WORD:
-            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellLatticeLink:
-            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvP:
-            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvMat:
             mv_mat_epilogue(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid); break;
           case ED_CELL_LINEAR_OUT:
             linear_out_epilogue(p, st, tacc, tfull + acc, par, row_tile, tid); break;
           default:
-            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
         }
         ED_TRACE(p, s, 5, tid == 0 && t == 0);
         tc_fence_before();
@@ -1335,7 +1396,49 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       }
       asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");  // sbias reused by the next step
       if (tid == 0) stamp_step(p, s);
-    } else if (warp == 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
+  for (int s = 0; s < p.num_steps; ++s) {
+    const DevStep st = p.steps[s];
+    const int T = step_items(st, h);
+    const int t0 = first_item(off);
+    off = (off + static_cast<uint32_t>(T)) % static_cast<uint32_t>(G);
+    if (t0 >= T) continue;  // no work for this CTA in this step
+    ED_TRACE(p, s, 0, tid == 0 && t0 == 0);
+    if (!is_umma_cell(st.cell)) {
+      if (st.cell == ED_CELL_MVRNN_INTERNAL) {  // ---- MV-RNN matvecs: one CTA per item ----
+        __syncthreads();  // sbias / swout are free (previous step's epilogue done)
+        mv_vec_items<__nv_bfloat16>(p, st, t0, G, sbias, swout);
+        if (tid == 0) stamp_step(p, s);
+        continue;
+      }
+      // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
+      const int C = st.gates;
+      const bool in_smem = C * h * 4 <= kWoutBytes;
+      if (in_smem) {  // 16 B cp.async per piece (no register staging)
+        const float *W = static_cast<const float *>(step_W(p, st));
+        const uint32_t sw = smem_u32(swout);
+        for (int q = tid; q < C * h / 4; q += kThreadsTC) cp_async16(sw + 16u * q, W + 4 * q);
+        cp_async_commit();
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      if (p.trace && tid == 0) p.trace[p.num_steps * 64 + blockIdx.x * 4 + 1] = globaltimer();
+      const float *Ws = in_smem ? swout : static_cast<const float *>(step_W(p, st));
+      for (int t = t0; t < T; t += G) linear_out_rows_bf16(p, st, static_cast<long>(t) * kSimtRows + 2 * warp, Ws);
+      if (p.trace && lane == 0) atomicMax(p.trace + p.num_steps * 64 + blockIdx.x * 4 + 2, globaltimer());
+      __syncthreads();  // swout is reused by the next SIMT step
+      if (tid == 0) stamp_step(p, s);
+      continue;
+    }
+    const int ncols = st.cell == ED_CELL_LINEAR_OUT ? 16 : st.gates * st.units;
+    const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
+    uint32_t abytes = kAStage;
+    const int kps = step_kps(st, kc_total, &abytes);
+    const uint32_t boff = kps > 1 ? kps * abytes : static_cast<uint32_t>(kAStage);  // B region of a stage
+    const uint32_t bchunk = static_cast<uint32_t>(ncols) * 128u;
+if (warp == 4) {
       // ---------------- MMA issuer ----------------
       for (int t = t0; t < T; t += G) {
         const uint32_t acc = pipe.ti & 1u;
@@ -1535,6 +1638,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
         if (lt == 0) ED_TRACE(p, s, 2, t == 0);
       }
     }
+  }
   }
   tc_fence_before();
   __syncthreads();

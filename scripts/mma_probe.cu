@@ -16,8 +16,9 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
          (2ull << 61);
 }
+__device__ int g_m = 128;  // MMA M (128 or 64)
 __device__ __forceinline__ uint32_t idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(g_m >> 4) << 24);
 }
 
 __global__ void probe(int n, int nmma, int nacc, unsigned long long *out) {
@@ -113,8 +114,11 @@ int main() {
   unsigned long long *out, h[4];
   cudaMalloc(&out, 64);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  for (int mm : {128, 64}) {
+  cudaMemcpyToSymbol(g_m, &mm, sizeof(int));
+  printf("M = %d\n", mm);
   for (int n : {32, 64, 80, 128, 160, 256})
-    for (int nacc : {-1, 0})
+    for (int nacc : {-1})
       for (int nmma : {16, 64}) {
         if (n * nacc > 512) continue;
         probe<<<1, 128, 70000>>>(n, nmma, nacc, out);
@@ -123,5 +127,6 @@ int main() {
         printf("N %3d acc %d mma %2d: issue %5.1f ns/mma, done %6.1f ns/mma (%.0f ns total)\n", n, nacc, nmma,
                double(h[2]) / nmma, double(h[3]) / nmma, double(h[3]));
       }
+  }
   return 0;
 }

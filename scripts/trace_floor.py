@@ -35,6 +35,6 @@ end = np.maximum.accumulate(ts)
 for s in range(nb):
     base = end[s]
     rel = lambda k: int(t[s, k] - base) if t[s, k] else None
-    print(s, [rel(k) for k in (0, 1, 2, 3, 4, 6, 5)], "|", int(ts[s + 1] - base))
+    print(s, [rel(k) for k in (0, 1, 2, 3, 4, 6, 10, 11, 12, 13, 7, 8, 9, 5)], "|", int(ts[s + 1] - base))
     if len(sys.argv) > 1:
         print("   mma", [rel(k) for k in range(24, 32)])

@@ -232,3 +232,75 @@ def test_mvrnn_rejects_bad_hidden():
     g = W.treefc(2, (2, 4), 8, "fp32", cfg=4).graphs
     with pytest.raises(E.EdError):
         E.ed_plan(g, t, E.fsm_from_priority([0], 1))
+
+
+_CODE = {v: k for k, v in E.STATUS.items()}
+
+
+def _execute_host_checks(plan, sets):
+    """ed_execute's host-side argument checks run before any CUDA call, so they are testable here
+    with dummy (never dereferenced) pointers and a dummy 1024-aligned workspace address."""
+    arr = (E.ed_weight_set_t * len(sets))(*sets)
+    w = E.ed_weights_t(len(sets), arr)
+    io = E.ed_io_t(None, None)
+    ws = ctypes.c_void_p(1 << 40)
+    return E.LIB.ed_execute(plan.handle, ctypes.byref(w), ctypes.byref(io), ws, plan.info["workspace_bytes"], None)
+
+
+def _dummy_set(emb_rows=0, emb2_rows=0, W2=True):
+    p = 1 << 41
+    return E.ed_weight_set_t(p, p, p if W2 else None, p if W2 else None, p if emb_rows else None,
+                             p if emb2_rows else None, None, emb_rows, emb2_rows)
+
+
+def test_external_inputs_only_where_a_table_backs_them():
+    """External ids (-1 - id) are rows of a weight set's table: TreeFC / MV-RNN children (emb) and a
+    lattice word's end char (slot 1, emb2).  Elsewhere (a TreeLSTM child, a variadic word input of a
+    lattice char) the kernel would index H with a negative row: the scheduler still plans the graph
+    (Alg. 1 is generic), ed_execute refuses it (ED_E_UNSUPPORTED) before touching the device."""
+    lstm = W.treelstm(2, (2, 4), 64, "bf16", cfg=5)
+    g = lstm.graphs[0]
+    bad_in = g.in_idx.copy()
+    internal = [v for v in range(g.num_nodes) if lstm.types[g.type[v]].kind == "treelstm_internal"][0]
+    bad_in[g.in_off[internal]] = -1 - 3
+    bad = W.Graph(g.type, g.in_off, bad_in, g.ext, g.root)
+    plan = E.ed_plan([bad], lstm.types, E.fsm_from_priority(lstm.priority, 3))
+    sets = [_dummy_set(emb_rows=10000), _dummy_set(), _dummy_set()]
+    assert _execute_host_checks(plan, sets) == _CODE["ED_E_UNSUPPORTED"]
+    assert b"external" in E.LIB.ed_last_error()
+    lat = W.lattice(6, (8, 14), 64, "bf16")
+    for gl in lat.graphs:
+        chars_with_words = [v for v in range(gl.num_nodes) if gl.type[v] == 0 and gl.in_off[v + 1] - gl.in_off[v] > 1]
+        if chars_with_words:
+            v = chars_with_words[0]
+            li = gl.in_idx.copy()
+            li[gl.in_off[v] + 1] = -1 - 2                          # variadic word slot
+            badl = W.Graph(gl.type, gl.in_off, li, gl.ext, gl.root)
+            p2 = E.ed_plan([badl], lat.types, E.fsm_from_priority(lat.priority, 2))
+            assert _execute_host_checks(p2, [_dummy_set(4096), _dummy_set(16384, 4096)]) == _CODE["ED_E_UNSUPPORTED"]
+            break
+    else:
+        pytest.fail("no lattice char with a word input")
+
+
+def test_execute_checks_token_ids_and_weight_pointers():
+    """Every token / external id a plan reads must be < the table's row count; W, b (and W2, b2 for
+    the tagger and lattice word cells) must be non-null."""
+    wl = W.lattice(6, (8, 14), 64, "bf16")
+    plan = E.ed_plan(wl.graphs, wl.types, E.fsm_from_priority(wl.priority, 2))
+    max_tok = max(int(g.ext[v]) for g in wl.graphs for v in range(g.num_nodes) if g.type[v] == 0)
+    max_word = max(int(g.ext[v]) for g in wl.graphs for v in range(g.num_nodes) if g.type[v] == 1)
+    ok_sets = [_dummy_set(max_tok + 1), _dummy_set(max_word + 1, 4096)]
+    # all checks pass: the call gets as far as the device (none here -> a CUDA error, not a check)
+    assert _execute_host_checks(plan, ok_sets) == _CODE["ED_E_CUDA"]
+    assert _execute_host_checks(plan, [_dummy_set(max_tok), ok_sets[1]]) == _CODE["ED_E_INVALID_ARG"]
+    assert b"emb" in E.LIB.ed_last_error()
+    assert _execute_host_checks(plan, [ok_sets[0], _dummy_set(max_word)]) == _CODE["ED_E_INVALID_ARG"]
+    assert _execute_host_checks(plan, [ok_sets[0], _dummy_set(max_word + 1, 4096, W2=False)]) == _CODE["ED_E_INVALID_ARG"]
+    assert b"W2" in E.LIB.ed_last_error()
+    # external child words of TreeFC index emb of the internal op's weight set
+    fc = W.treefc(6, (2, 9), 64, "bf16", cfg=4)
+    pfc = E.ed_plan(fc.graphs, fc.types, E.fsm_from_priority(fc.priority, len(fc.types)))
+    max_w = max(-1 - int(x) for g in fc.graphs for x in g.in_idx if x < 0 and x != -(2 ** 31))
+    assert _execute_host_checks(pfc, [_dummy_set(max_w + 1)] + [_dummy_set()] * (len(fc.types) - 1)) == _CODE["ED_E_CUDA"]
+    assert _execute_host_checks(pfc, [_dummy_set(max_w)] + [_dummy_set()] * (len(fc.types) - 1)) == _CODE["ED_E_INVALID_ARG"]
