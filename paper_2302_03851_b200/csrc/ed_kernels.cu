@@ -3,20 +3,21 @@
 // One persistent cooperative kernel walks the whole FSM batch schedule (PAPER Alg. 1,
 // P:75-87): for every batch ("step") it reads operand rows (gathered by index, or one contiguous
 // block where the layout plan made them adjacent), runs the cell's dense contraction,
-// applies the fused gate epilogue and stores the results as one contiguous row block; a grid-wide
-// barrier separates dependent steps, replacing the per-batch kernel launches of the paper's
-// DyNet executor.
+// applies the fused gate epilogue and stores the results as one contiguous row block.  Dependent
+// steps are ordered by per-row readiness counters (release / acquire), not by kernel launches or
+// grid barriers: this replaces the per-batch kernel launches of the paper's DyNet executor.
 //
-//   bf16 path (ed_persistent_bf16): single-GEMM cells on the 5th-gen tensor cores —
-//     warps 0-3  epilogue: tcgen05.ld TMEM -> registers, gates in fp32, vector stores
-//     warp  4    MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128)
+//   bf16 path (ed_persistent_bf16): every cell's contraction on the 5th-gen tensor cores —
+//     warps 0-3  epilogue (setmaxnreg 232): tcgen05.ld TMEM -> registers, gates in fp32, vector stores
+//     warp  4    MMA issuer: tcgen05.mma.cta_group::1.kind::f16 (M=128), elect.sync issue
 //     warp  5    weight loader: cp.async.bulk of pre-swizzled weight tiles (complete_tx)
-//     warps 6-11 operand loaders: TMA 128-row box for CONTIG operands, 16 B cp.async row gathers
-//                otherwise (192 threads), into 128B-swizzled A tiles
+//     warps 6-11 operand loaders: TMA 128-row box for CONTIG / staged operands, 16 B cp.async row
+//                gathers otherwise (192 threads), into 128B-swizzled A tiles
 //     4-stage smem ring (mbarrier full/empty), 2 TMEM accumulators (2 x 256 columns).
-//     Narrow cells (output linear, N = C) run as a warp-per-row SIMT phase (HBM-bound).
+//     The output linear O runs as an N = 16 tensor-core tile; the tagger output and the MV-RNN
+//     matvecs are SIMT phases of all warps.
 //   fp32 path (ed_persistent_f32): FFMA SIMT for every cell (1e-4 parity path; single-pass TF32
-//     and approximate transcendentals cannot meet 1e-4).
+//     and approximate transcendentals cannot meet 1e-4, A-20).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -42,10 +43,9 @@ constexpr int kAStage = kTileM * 128;        // 16 KB
 constexpr int kBStage = 256 * 128;           // 32 KB (N tile <= 256)
 constexpr int kStageBytes = kAStage + kBStage;
 constexpr int kRowTab = kTileM * 2 * 8;      // row pointers per tile (2 segments)
-constexpr int kEntTab = 0;
 constexpr int kBiasBytes = 5 * 512 * 4;           // G * h fp32 (G * h <= 2560)
 constexpr int kWoutBytes = 12 * 1024;             // output-linear weights [C][h] fp32 (else read from L2)
-constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes + kWoutBytes + 256;
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kBiasBytes + kWoutBytes + 256;
 constexpr int kEpiThreads = 128;
 // setmaxnreg budgets (multiples of 8): 128 x kEpiRegs + 256 x kProdRegs <= 64K registers per SM
 #ifndef ED_EPI_REGS
@@ -123,15 +123,6 @@ __device__ __forceinline__ void tma_row_box_elect(void *dst, const CUtensorMap *
       "@e cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(
           smem_u32(dst)),
       "l"(m), "r"(col), "r"(row), "r"(smem_u32(bar))
-      : "memory");
-}
-// TMA tile::gather4: 4 rows (r0..r3) x 64 cols at col -> 4 consecutive 128 B smem rows (128B swizzle)
-__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *m, int col, int r0, int r1, int r2, int r3,
-                                            uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-      "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
-      "l"(m), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
@@ -902,18 +893,6 @@ template <> struct CellCfg<kCellLatticeLink> { static constexpr int G = 1, U = 2
 template <> struct CellCfg<ED_CELL_TAGGER> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 template <> struct CellCfg<kCellMvP> { static constexpr int G = 1, U = 256, NC = 0, NH = 0; };
 
-// Row pointers (per K segment) of the 128 rows of a row tile; rows past m repeat the last valid row.
-__device__ __forceinline__ void build_row_table(const KParams &p, const DevStep &st, int row_tile, int nseg, int lt,
-                                                const void **tab) {
-  for (int r = lt; r < kTileM; r += kLoaderThreads) {
-    const int i = row_tile * kTileM + r;
-    const int iv = i < st.m ? i : (st.m - 1);
-#pragma unroll
-    for (int sg = 0; sg < 2; ++sg)
-      sts_ptr(tab + r * 2 + sg, sg < nseg ? static_cast<const void *>(segment_row<__nv_bfloat16>(p, st, sg, iv)) : p.H);
-  }
-}
-
 // Hidden units of column tile ct (the last tile of a row may be narrower: h need not divide by U).
 __device__ __forceinline__ int tile_units(const DevStep &st, int h, int ct) { return min(st.units, h - ct * st.units); }
 // MMA N of a column tile: G * units, or 16 for the output linear (C <= 16 classes, zero-padded W_O)
@@ -1260,9 +1239,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stages = smem;
   const void **rowtab = reinterpret_cast<const void **>(smem + kStages * kStageBytes);  // [2][128][2] row ptrs
-  float *sbias = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab + kEntTab);
-  float *swout = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + 2 * kRowTab + kEntTab + kBiasBytes +
+  float *sbias = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab);
+  float *swout = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab + kBiasBytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + 2 * kRowTab + kBiasBytes +
                                                 kWoutBytes);
   uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = bars + 2 * kStages + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);

@@ -302,12 +302,28 @@ class Plan:
         return LIB.ed_execute_launch_count(self.handle)
 
 
+class GraphBatch:
+    """A minibatch of instance graphs packed once into the C ABI's layout (four concatenated int32
+    CSR arrays + the ed_graph_t records pointing into them): what a data loader hands to ed_plan.
+    Immutable; ed_plan on a GraphBatch does no per-call marshalling of the graphs."""
+
+    def __init__(self, graphs):
+        self._keep = []
+        self.num_graphs = len(graphs)
+        self.garr = _graph_arrays(graphs, self._keep)
+
+
 def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: int = ED_ENC_SORT,
             layout: int = ED_LAYOUT_SCHEDULE_ORDER, staging: int = 0) -> Plan:
-    """graphs: objects with numpy fields type/in_off/in_idx/ext and int root (workloads.Graph);
-    types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype."""
+    """graphs: a GraphBatch, or objects with numpy fields type/in_off/in_idx/ext and int root
+    (workloads.Graph); types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype.
+    The C call runs without the GIL (ctypes), so several host threads can plan concurrently."""
     keep = []
-    garr = _graph_arrays(graphs, keep)
+    if isinstance(graphs, GraphBatch):
+        garr, ngraphs = graphs.garr, graphs.num_graphs
+        keep.append(graphs)
+    else:
+        garr, ngraphs = _graph_arrays(graphs, keep), len(graphs)
     tarr = _type_array(types)
     earr = (ed_fsm_entry_t * max(len(fsm), 1))()
     for k, (key, act) in enumerate(fsm):
@@ -317,8 +333,27 @@ def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: in
     f = ed_fsm_t(encoder, len(fsm), earr, 0)
     opts = ed_plan_opts_t(layout, staging, (ctypes.c_int32 * 6)())
     h = ctypes.c_void_p()
-    _check(LIB.ed_plan(garr, len(graphs), tarr, len(types), ctypes.byref(f), ctypes.byref(opts), ctypes.byref(h)))
+    _check(LIB.ed_plan(garr, ngraphs, tarr, len(types), ctypes.byref(f), ctypes.byref(opts), ctypes.byref(h)))
     return Plan(h, len(types))
+
+
+class PlanPipeline:
+    """Plans upcoming minibatches on host threads while the GPU executes the current one (the
+    paper's construction + scheduling time, Fig. 6, taken off the critical path of a serving loop).
+    submit(batch) -> concurrent.futures.Future[Plan]; results are consumed in submission order by the
+    caller, which executes them on its stream.  ed_plan holds no global state, so plans of different
+    minibatches are independent."""
+
+    def __init__(self, types, fsm, workers: int, **plan_kw):
+        import concurrent.futures as cf
+        self.types, self.fsm, self.plan_kw = types, fsm, plan_kw
+        self.pool = cf.ThreadPoolExecutor(max_workers=max(1, workers))
+
+    def submit(self, batch):
+        return self.pool.submit(ed_plan, batch, self.types, self.fsm, **self.plan_kw)
+
+    def close(self):
+        self.pool.shutdown(wait=True)
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:
