@@ -108,6 +108,34 @@ def paper_copy_kernels(m: Merged, sched, row: Sequence[int]) -> Tuple[int, int]:
     return G, S
 
 
+def executor_copy_split(m: Merged, sched, row: Sequence[int]) -> Tuple[int, int]:
+    """Gather / scatter kernels of an executor that orders each batch's members by the memory
+    position of their slot-0 source (PAPER Fig. 3(b): B1 is written [x4, x5] = alpha([x1, x3],
+    [x2, x1]) and B2 [x8, x6, x7] = sigma([x3, x4, x5]) -- in both batches the members follow their
+    first source operand; reading A-25b).  A member whose slot-0 input is not a node keeps
+    its result position.  Under that order every source operand that is not consecutive-ascending in
+    memory costs one gather, a result operand that is not costs one scatter.  Returns (gathers,
+    scatters)."""
+    G = S = 0
+    for _, members in sched:
+        members = list(members)
+        ns = fixed_slots(m, members)
+
+        def key(v):
+            ins = m.inputs[v]
+            if ins and ins[0][0] == "n":
+                return (0, row[ins[0][1]], row[v])
+            return (1, row[v], row[v])
+        ordered = sorted(members, key=key)
+        if contig_base([("n", v) for v in ordered], row) < 0:
+            S += 1
+        for j in range(ns):
+            op = source_operand(m, ordered, j)
+            if all(e is not None and e[0] == "n" for e in op) and contig_base(op, row) < 0:
+                G += 1
+    return G, S
+
+
 def copy_bytes(m: Merged, sched, row: Sequence[int], row_bytes: int) -> Tuple[int, int]:
     """Bytes a DyNet-style executor would move (SURVEY §8(d) "bytes avoided"): 2 x rows x
     row_bytes per non-contiguous source operand (gather = read + write) and the same per

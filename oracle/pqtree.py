@@ -277,10 +277,11 @@ def subtree_constraints(T: PQTree, O: List[int]) -> List[Tuple[int, ...]]:
     return out
 
 
-def plan_pq_layout(m: Merged, sched, fixed_slots: Sequence[int]) -> Tuple[List[int], List[bool]]:
+def plan_pq_layout(m: Merged, sched, fixed_slots: Sequence[int], trace: Dict = None) -> Tuple[List[int], List[bool]]:
     """Returns (row_of_node, kept per batch): kept = the batch passed adjacency, broadcast and
     alignment (its constrained operands are contiguous and aligned); fixed_slots[t] = fixed input
-    slots of type t."""
+    slots of type t.  trace (optional dict) receives "pass1" = kept per batch after the
+    transactional source-constraint pass (test hook; no effect on the result)."""
     ops = batch_operands(m, sched, fixed_slots)
     T = PQTree(range(m.n))
     if m.n == 0:
@@ -298,6 +299,8 @@ def plan_pq_layout(m: Merged, sched, fixed_slots: Sequence[int]) -> Tuple[List[i
         except Fail:
             T.root = saved
             alive[b] = False
+    if trace is not None:
+        trace["pass1"] = list(alive)
     for _ in range(MAX_SWEEPS):                 # BroadcastConstraint
         any_change = False
         for b, o in enumerate(ops):

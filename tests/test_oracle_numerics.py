@@ -299,3 +299,61 @@ def test_latticegru_char_max_pools_word_states():
     out = cells.latticegru_char(p, x, hp, [w1, w2])
     np.testing.assert_array_equal(out[:3], [10.0, 10.0, 10.0])
     np.testing.assert_allclose(out[3], g[3], atol=1e-14)
+
+
+def test_mvrnn_cross_application_by_hand():
+    """Socher et al. 2012: p = tanh(W [B a; A b] + b_W), P = W_M [A; B] -- each
+    child's vector is transformed by the OTHER child's matrix, and the matrices stack A over B.
+    Non-symmetric A != B and selector weights make every plausible swap visible; values by hand."""
+    h = 2
+    a, A = np.array([0.1, 0.2]), np.array([[1.0, 2.0], [0.0, 1.0]])
+    b, B = np.array([0.3, -0.4]), np.array([[0.0, 1.0], [-1.0, 0.0]])
+    I, Z = np.eye(h), np.zeros((h, h))
+    # W = [I | 0] selects B a = (0.2, -0.1); W = [0 | I] selects A b = (0.3 - 0.8, -0.4) = (-0.5, -0.4)
+    pv, P = cells.mvrnn_internal({"W": np.hstack([I, Z]), "b": np.zeros(h), "WM": np.hstack([I, Z])}, a, A, b, B)
+    np.testing.assert_allclose(pv, np.tanh([0.2, -0.1]), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(P, A, rtol=0, atol=0)                       # W_M = [I | 0]: P = A
+    pv, P = cells.mvrnn_internal({"W": np.hstack([Z, I]), "b": np.array([0.05, 0.0]), "WM": np.hstack([Z, I])},
+                                 a, A, b, B)
+    np.testing.assert_allclose(pv, np.tanh([-0.5 + 0.05, -0.4]), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(P, B, rtol=0, atol=0)                       # W_M = [0 | I]: P = B
+    _, P = cells.mvrnn_internal({"W": np.hstack([I, I]), "b": np.zeros(h), "WM": np.hstack([I, 2 * I])}, a, A, b, B)
+    np.testing.assert_allclose(P, A + 2 * B, rtol=0, atol=0)
+
+
+def test_tagger_equals_torch_linear_tanh_linear():
+    """BiLSTM tagger head: y = W_2 tanh(W_1 [h_f; h_b] + b_1) + b_2 is
+    torch.nn.Sequential(Linear(2h, h), Tanh(), Linear(h, C)) on the concatenated states."""
+    gen = np.random.default_rng(21)
+    h, C = 5, 3
+    p = {"W": _rand(gen, h, 2 * h), "b": _rand(gen, h), "W2": _rand(gen, C, h), "b2": _rand(gen, C)}
+    hf, hb = _rand(gen, h), _rand(gen, h)
+    net = torch.nn.Sequential(torch.nn.Linear(2 * h, h), torch.nn.Tanh(), torch.nn.Linear(h, C))
+    with torch.no_grad():
+        net[0].weight.copy_(torch.tensor(p["W"])); net[0].bias.copy_(torch.tensor(p["b"]))
+        net[2].weight.copy_(torch.tensor(p["W2"])); net[2].bias.copy_(torch.tensor(p["b2"]))
+        yt = net(torch.tensor(np.concatenate([hf, hb]))[None])[0].numpy()
+    np.testing.assert_allclose(cells.tagger(p, hf, hb), yt, rtol=0, atol=1e-14)
+    # the forward state feeds the first h columns: swapping the directions changes the logits
+    assert np.max(np.abs(cells.tagger(p, hb, hf) - yt)) > 1e-3
+
+
+def test_treegru_internal_mirrored_spine_equals_grucell():
+    """h_l = 0, U_{.l} = 0 and b_nl = 0: internal = GRUCell(0, h_r), which pins the right-child
+    path the left spine cannot see: r_r, U_nr and the h_r term of z (h_l + h_r)."""
+    gen = np.random.default_rng(22)
+    h = 4
+    W = _rand(gen, 5 * h, 2 * h)
+    W[:, :h] = 0                         # no left-child columns
+    b = _rand(gen, 5 * h)
+    b[3 * h:4 * h] = 0                   # a_l = U_nl h_l + b_nl = 0
+    p = {"W": W, "b": b}
+    hr = _rand(gen, h)
+    out = cells.treegru_internal(p, np.zeros(h), hr)
+    cell = torch.nn.GRUCell(h, h)
+    with torch.no_grad():  # h' = (1-z) n + z h; n = tanh(r * (W_hn h + b_hn)); gates [r, z, n]
+        cell.weight_ih.zero_(); cell.bias_ih.zero_()
+        cell.weight_hh.copy_(torch.tensor(np.concatenate([W[2 * h:3 * h, h:], W[:h, h:], W[4 * h:, h:]])))
+        cell.bias_hh.copy_(torch.tensor(np.concatenate([b[2 * h:3 * h], b[:h], b[4 * h:]])))
+        ht = cell(torch.zeros(1, h), torch.tensor(hr)[None])
+    np.testing.assert_allclose(out, ht[0].numpy(), rtol=0, atol=1e-14)
