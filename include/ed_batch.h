@@ -70,6 +70,9 @@ typedef int32_t ed_status_t;
 
 #define ED_ENC_SORT 0   /* E_sort: frontier types by descending count, ties ascending id */
 #define ED_ENC_BASE 1   /* E_base: ascending set of frontier types                                 */
+#define ED_ENC_MAX  2   /* E_max: (E_base, the most frequent frontier type); as an entry key:
+                           the ascending type set followed by that type (key_len = |set| + 1;
+                           count ties to the lowest type id)                                        */
 
 #define ED_FALLBACK_KEY0 0  /* table miss or action not ready: take key[0] (reading A-3) */
 
@@ -116,7 +119,7 @@ typedef struct {
 } ed_fsm_entry_t;
 
 typedef struct {
-  int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE */
+  int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE | ED_ENC_MAX */
   int32_t num_entries;
   const ed_fsm_entry_t *entries;
   int32_t fallback;      /* ED_FALLBACK_KEY0 */
@@ -129,8 +132,22 @@ typedef struct {
                             contiguous operand block of the consuming batch, read by TMA);
                             ED_STAGING_OFF (1): every non-contiguous operand is gathered row by
                             row.  Results are bitwise identical. */
-  int32_t reserved[6];   /* must be 0 */
+  int32_t policy;        /* batching policy (PAPER P:107, P:436 comparators; Fig. 8):
+                            ED_POLICY_FSM (0): Alg. 1 with the FSM table (fsm), the default;
+                            ED_POLICY_DEPTH: TF-Fold depth-based: one batch per (topological
+                              depth, type), ascending depth then type id (fsm ignored);
+                            ED_POLICY_AGENDA: DyNet agenda-based Alg. 1: the ready type with the
+                              smallest mean depth over all nodes of the type, ties to the lower id;
+                            ED_POLICY_SC: sufficient-condition heuristic Alg. 1: argmax of Eq. 1's
+                              second term |Frontier_a(G_t)| / |Frontier(G^a_t)| (A-1),
+                              ties to the larger ready count, then the lower id.
+                            Depth of an op = 1 + max depth of its node inputs (raw inputs: 0). */
+  int32_t reserved[5];   /* must be 0 */
 } ed_plan_opts_t;
+#define ED_POLICY_FSM    0
+#define ED_POLICY_DEPTH  1
+#define ED_POLICY_AGENDA 2
+#define ED_POLICY_SC     3
 
 typedef struct ed_plan_s ed_plan_t;  /* opaque plan handle */
 
@@ -259,7 +276,7 @@ ed_status_t ed_workspace_release(const void *workspace);
 /* ---------------------------------------------------------------------------------------------
  * Learning the FSM (PAPER §2.3 "Using RL to Learn the FSM"; §5.3): tabular
  * N-step Q-learning over the instance graphs, one instance per episode (episodes cycle over the
- * graphs).  State = E(G_t) (ED_ENC_SORT or ED_ENC_BASE), action = the next batch's type (all
+ * graphs).  State = E(G_t) (ED_ENC_SORT, ED_ENC_BASE or ED_ENC_MAX), action = the next batch's type (all
  * ready nodes of it, Alg. 1), reward Eq. 1 r = -1 + alpha * |Frontier_a(G_t)| / |Frontier(G^a_t)|
  * (the ratio read as in DESIGN.md A-1).  After each episode, for t = 0..T-1 in order:
  *   Q(S_t,a_t) += lr * (sum_{i<N, t+i<T} r_{t+i} + [t+N<T] max_b Q(S_{t+N},b) - Q(S_t,a_t))
@@ -274,7 +291,7 @@ ed_status_t ed_workspace_release(const void *workspace);
  * the final Q; fewest batches, earliest on ties).
  * Host only; deterministic for a given seed; no CUDA call. ------------------------------------ */
 typedef struct {
-  int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE                                            */
+  int32_t encoder;       /* ED_ENC_SORT | ED_ENC_BASE | ED_ENC_MAX                               */
   int32_t n_steps;       /* N >= 1 (bootstrapping horizon)                                        */
   int32_t max_episodes;  /* paper: 1000                                                   */
   int32_t check_every;   /* paper: 50                                                     */
@@ -312,7 +329,7 @@ ed_status_t ed_fsm_learned_info(const ed_fsm_learned_t *fl, ed_fsm_learned_info_
  * entries and keys are owned by fl and valid until ed_fsm_learned_destroy. */
 ed_status_t ed_fsm_learned_table(const ed_fsm_learned_t *fl, ed_fsm_t *out);
 /* Q entry k in (state key lexicographic, action ascending) order: key[*key_len] (capacity
- * num_types), action and value. */
+ * num_types + 1: an E_max key is the type set followed by its most frequent type), action and value. */
 ed_status_t ed_fsm_learned_q(const ed_fsm_learned_t *fl, int64_t k, int32_t *key, int32_t *key_len,
                              int32_t *action, double *q);
 /* Checkpoint c: episode count and greedy batch total at that checkpoint. */

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -292,28 +293,80 @@ static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, i
 // ------------------------------------------------------------------------------------------------
 // Alg. 1 with E_sort / E_base + table lookup; fallback key[0] (A-3)
 // ------------------------------------------------------------------------------------------------
-static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
+static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm, int policy) {
   const int nt = static_cast<int>(pl->types.size());
   const int64_t V = pl->V;
+  // comparators: topological depth (1 + max over node inputs; raw inputs 0)
+  std::vector<int32_t> depth;
+  std::vector<double> mean_depth;
+  std::vector<int32_t> sc_seq;
+  if (policy == ED_POLICY_DEPTH || policy == ED_POLICY_AGENDA) {
+    depth.assign(V, 0);
+    std::vector<int32_t> d(pl->indeg), q;
+    q.reserve(V);
+    for (int64_t v = 0; v < V; ++v)
+      if (d[v] == 0) q.push_back(static_cast<int32_t>(v));
+    for (size_t hh = 0; hh < q.size(); ++hh) {
+      const int32_t v = q[hh];
+      int32_t dv = 0;
+      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+        if (pl->in_idx[k] >= 0) dv = std::max(dv, depth[pl->in_idx[k]]);
+      depth[v] = dv + 1;
+      for (int k = pl->coff[v]; k < pl->coff[v + 1]; ++k)
+        if (--d[pl->cons[k]] == 0) q.push_back(pl->cons[k]);
+    }
+  }
+  if (policy == ED_POLICY_AGENDA) {  // mean depth over all nodes of the type (A-22)
+    std::vector<int64_t> sum(nt, 0), cnt(nt, 0);
+    for (int64_t v = 0; v < V; ++v) {
+      sum[pl->gtype[v]] += depth[v];
+      ++cnt[pl->gtype[v]];
+    }
+    mean_depth.assign(nt, std::numeric_limits<double>::infinity());
+    for (int t = 0; t < nt; ++t)
+      if (cnt[t]) mean_depth[t] = static_cast<double>(sum[t]) / static_cast<double>(cnt[t]);
+  }
+  if (policy == ED_POLICY_SC) {  // the type sequence of the SC chooser on the merged graph
+    ed::RlGraph g;
+    g.n = static_cast<int32_t>(V);
+    g.type = pl->gtype;
+    g.pred_off.assign(1, 0);
+    for (int64_t v = 0; v < V; ++v) {
+      std::vector<int32_t> pr;
+      for (int k = pl->in_off[v]; k < pl->in_off[v + 1]; ++k)
+        if (pl->in_idx[k] >= 0) pr.push_back(pl->in_idx[k]);
+      std::sort(pr.begin(), pr.end());
+      pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+      g.preds.insert(g.preds.end(), pr.begin(), pr.end());
+      g.pred_off.push_back(static_cast<int32_t>(g.preds.size()));
+    }
+    sc_seq = ed::sc_type_sequence(g, nt);
+  }
   std::map<std::vector<int32_t>, int32_t> table;
   int encoder = ED_ENC_SORT;
   if (fsm) {
     encoder = fsm->encoder;
-    if (encoder != ED_ENC_SORT && encoder != ED_ENC_BASE) return fail(ED_E_FSM, "unknown encoder");
+    if (encoder != ED_ENC_SORT && encoder != ED_ENC_BASE && encoder != ED_ENC_MAX) return fail(ED_E_FSM, "unknown encoder");
     if (fsm->fallback != ED_FALLBACK_KEY0) return fail(ED_E_FSM, "unknown fallback");
     if (fsm->num_entries > 0 && !fsm->entries) return fail(ED_E_FSM, "null entries");
     for (int e = 0; e < fsm->num_entries; ++e) {
       const ed_fsm_entry_t &en = fsm->entries[e];
-      if (en.key_len <= 0 || en.key_len > nt || !en.key) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": bad key");
-      std::vector<int32_t> key(en.key, en.key + en.key_len);
+      const int set_len = encoder == ED_ENC_MAX ? en.key_len - 1 : en.key_len;  // E_max: set + argmax type
+      if (set_len <= 0 || set_len > nt || !en.key) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": bad key");
+      std::vector<int32_t> key(en.key, en.key + set_len);
+      if (encoder == ED_ENC_MAX) {
+        if (!std::is_sorted(key.begin(), key.end()) || std::find(key.begin(), key.end(), en.key[set_len]) == key.end())
+          return fail(ED_E_FSM, "entry " + std::to_string(e) + ": E_max key must be an ascending set followed by one of its types");
+      }
       std::vector<int32_t> sorted_key = key;
       std::sort(sorted_key.begin(), sorted_key.end());
-      for (int k = 0; k < en.key_len; ++k) {
+      for (int k = 0; k < set_len; ++k) {
         if (key[k] < 0 || key[k] >= nt) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": key type out of range");
         if (k > 0 && sorted_key[k] == sorted_key[k - 1]) return fail(ED_E_FSM, "entry " + std::to_string(e) + ": repeated type in key");
       }
       if (std::find(key.begin(), key.end(), en.action) == key.end())
         return fail(ED_E_FSM, "entry " + std::to_string(e) + ": action not present in its key");
+      if (encoder == ED_ENC_MAX) key.push_back(en.key[set_len]);
       table[key] = en.action;
     }
   }
@@ -328,7 +381,7 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
   pl->members.clear();
   pl->members.reserve(V);
   std::vector<int32_t> key, order(nt);
-  int64_t done = 0;
+  int64_t done = policy == ED_POLICY_DEPTH ? V : 0;  // depth-based: grouped below, no Alg. 1
   while (done < V) {
     key.clear();
     for (int t = 0; t < nt; ++t)
@@ -336,10 +389,22 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
     if (key.empty()) return fail(ED_E_CYCLE, "no ready node (internal)");
     std::vector<int32_t> skey = key;  // E_sort: descending count, ties ascending id
     std::stable_sort(skey.begin(), skey.end(), [&](int a, int b) { return ready[a].size() > ready[b].size(); });
-    const std::vector<int32_t> &lookup = encoder == ED_ENC_SORT ? skey : key;
+    std::vector<int32_t> mkey;
+    if (encoder == ED_ENC_MAX) {  // (E_base, most frequent type) = ascending set + skey[0]
+      mkey = key;
+      mkey.push_back(skey[0]);
+    }
+    const std::vector<int32_t> &lookup = encoder == ED_ENC_SORT ? skey : (encoder == ED_ENC_MAX ? mkey : key);
     int32_t act = -1;
-    auto it = table.find(lookup);
-    if (it != table.end()) act = it->second;
+    if (policy == ED_POLICY_FSM) {
+      auto it = table.find(lookup);
+      if (it != table.end()) act = it->second;
+    } else if (policy == ED_POLICY_AGENDA) {
+      for (int t : key)
+        if (act < 0 || mean_depth[t] < mean_depth[act]) act = t;
+    } else if (policy == ED_POLICY_SC) {
+      act = sc_seq[pl->batch_type.size()];
+    }
     if (act < 0 || ready[act].empty()) act = skey[0];
     std::vector<int32_t> batch;
     batch.swap(ready[act]);
@@ -354,6 +419,23 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm) {
     done += static_cast<int64_t>(batch.size());
     pl->batch_type.push_back(act);
     pl->batch_off.push_back(static_cast<int32_t>(pl->members.size()));
+  }
+  if (policy == ED_POLICY_DEPTH) {  // TF-Fold: one batch per (depth, type), ascending
+    std::vector<int64_t> keyv(V);
+    std::vector<int32_t> ord(V);
+    for (int64_t v = 0; v < V; ++v) {
+      keyv[v] = static_cast<int64_t>(depth[v]) * nt + pl->gtype[v];
+      ord[v] = static_cast<int32_t>(v);
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return keyv[a] < keyv[b]; });
+    pl->batch_type.clear();
+    pl->batch_off.assign(1, 0);
+    pl->members.assign(ord.begin(), ord.end());
+    for (int64_t k = 0; k < V; ++k)
+      if (k + 1 == V || keyv[ord[k + 1]] != keyv[ord[k]]) {
+        pl->batch_type.push_back(pl->gtype[ord[k]]);
+        pl->batch_off.push_back(static_cast<int32_t>(k + 1));
+      }
   }
   // App. B.3 lower bound: per type, the max number of type-t nodes on a path (= Depth(G^t)).
   // one pass over the schedule order (a topological order) with nt counters per node
@@ -768,8 +850,10 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   const int layout = opts ? opts->layout : ED_LAYOUT_SCHEDULE_ORDER;
   if (layout != ED_LAYOUT_SCHEDULE_ORDER && layout != ED_LAYOUT_PQ) return fail(ED_E_INVALID_ARG, "unknown layout");
   if (opts)
-    for (int k = 0; k < 6; ++k)
+    for (int k = 0; k < 5; ++k)
       if (opts->reserved[k] != 0) return fail(ED_E_INVALID_ARG, "opts.reserved must be 0");
+  if (opts && (opts->policy < ED_POLICY_FSM || opts->policy > ED_POLICY_SC))
+    return fail(ED_E_INVALID_ARG, "unknown batching policy");
   if (opts && opts->staging != ED_STAGING_AUTO && opts->staging != ED_STAGING_OFF)
     return fail(ED_E_INVALID_ARG, "unknown staging mode");
   ed_plan_t *pl = new (std::nothrow) ed_plan_t();
@@ -797,7 +881,7 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   ed_status_t st = validate_and_merge(pl, graphs, num_graphs);
   if (st != ED_OK) { delete pl; return st; }
   const double t1 = now_us();
-  st = schedule(pl, fsm);
+  st = schedule(pl, fsm, opts ? opts->policy : ED_POLICY_FSM);
   if (st != ED_OK) { delete pl; return st; }
   const double t2 = now_us();
   if (layout == ED_LAYOUT_PQ) {

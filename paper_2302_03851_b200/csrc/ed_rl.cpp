@@ -123,10 +123,16 @@ struct Env {
   // frontier types -> encoded key (E_sort: descending count, ties ascending id; E_base: ascending)
   void key(int encoder, std::vector<int32_t> *k) const {
     k->clear();
+    int best = -1;
     for (int t = 0; t < static_cast<int>(ready.size()); ++t)
-      if (!ready[t].empty()) k->push_back(t);
+      if (!ready[t].empty()) {
+        k->push_back(t);
+        if (best < 0 || ready[t].size() > ready[best].size()) best = t;  // ties: lowest id
+      }
     if (encoder == ED_ENC_SORT)
       std::stable_sort(k->begin(), k->end(), [&](int a, int b) { return ready[a].size() > ready[b].size(); });
+    else if (encoder == ED_ENC_MAX)
+      k->push_back(best);  // E_max = (E_base, argmax type): the set, then that type
   }
   double ratio(int a) const { return static_cast<double>(ready[a].size()) / static_cast<double>(gfront[a]); }
   void execute(int a) {
@@ -157,8 +163,9 @@ int greedy(const std::map<std::pair<std::vector<int32_t>, int32_t>, double> &q, 
   return best;
 }
 
+thread_local int g_encoder = ED_ENC_SORT;  // set by rl_train: an E_max key carries its argmax type last
 std::vector<int32_t> ascending(const std::vector<int32_t> &key) {
-  std::vector<int32_t> r(key);
+  std::vector<int32_t> r(key.begin(), key.end() - (g_encoder == ED_ENC_MAX ? 1 : 0));  // the ready types
   std::sort(r.begin(), r.end());
   return r;
 }
@@ -199,11 +206,34 @@ int64_t evaluate(const std::vector<RlGraph> &gs, const std::vector<Prepared> &Ps
 
 }  // namespace
 
+std::vector<int32_t> sc_type_sequence(const RlGraph &g, int nt) {
+  const Prepared P = prepare(g, nt);
+  Env env;
+  env.reset(g, P, nt);
+  std::vector<int32_t> seq;
+  while (env.left > 0) {
+    int best = -1;
+    double br = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      if (env.ready[t].empty()) continue;
+      const double r = env.ratio(t);
+      if (best < 0 || r > br || (r == br && env.ready[t].size() > env.ready[best].size())) {
+        best = t;
+        br = r;
+      }
+    }
+    seq.push_back(best);
+    env.execute(best);
+  }
+  return seq;
+}
+
 int rl_train(const std::vector<RlGraph> &gs, int nt, const ed_rl_config_t &cfg, RlResult *out) {
   if (gs.empty() || cfg.n_steps < 1 || cfg.max_episodes < 0 || cfg.check_every < 1 || cfg.eps_every < 1 ||
-      !(cfg.alpha >= 0.0) || !(cfg.lr > 0.0 && cfg.lr <= 1.0) || (cfg.encoder != ED_ENC_SORT && cfg.encoder != ED_ENC_BASE) ||
+      !(cfg.alpha >= 0.0) || !(cfg.lr > 0.0 && cfg.lr <= 1.0) || (cfg.encoder != ED_ENC_SORT && cfg.encoder != ED_ENC_BASE && cfg.encoder != ED_ENC_MAX) ||
       (cfg.episode_graph != ED_RL_EPISODE_INSTANCE && cfg.episode_graph != ED_RL_EPISODE_MERGED))
     return -1;
+  g_encoder = cfg.encoder;
   std::vector<Prepared> Ps;
   Ps.reserve(gs.size());
   out->lower_bound = 0;

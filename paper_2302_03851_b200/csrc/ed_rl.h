@@ -28,4 +28,9 @@ struct RlResult {
 // Returns 0 on success, -1 on a bad config.
 int rl_train(const std::vector<RlGraph> &graphs, int num_types, const ed_rl_config_t &cfg, RlResult *out);
 
+// Type of every batch of Alg. 1 run with the sufficient-condition chooser: argmax over the
+// ready types of |Frontier_a(G_t)| / |Frontier(G^a_t)|, ties to the larger ready count, then the
+// lower type id.
+std::vector<int32_t> sc_type_sequence(const RlGraph &g, int num_types);
+
 }  // namespace ed

@@ -19,10 +19,11 @@ LIB_PATH = os.environ.get("ED_BATCH_LIB") or os.path.join(_HERE, "libedbatch.so"
 ED_OK = 0
 ED_ZERO_INPUT = -(2 ** 31)
 ED_FP32, ED_BF16 = 0, 1
-ED_ENC_SORT, ED_ENC_BASE = 0, 1
+ED_ENC_SORT, ED_ENC_BASE, ED_ENC_MAX = 0, 1, 2
 ED_RL_EPISODE_INSTANCE, ED_RL_EPISODE_MERGED = 0, 1
 ED_LAYOUT_SCHEDULE_ORDER, ED_LAYOUT_PQ = 0, 1
 ED_STAGING_AUTO, ED_STAGING_OFF = 0, 1
+ED_POLICY_FSM, ED_POLICY_DEPTH, ED_POLICY_AGENDA, ED_POLICY_SC = 0, 1, 2, 3
 STATUS = {0: "ED_OK", -1: "ED_E_INVALID_ARG", -2: "ED_E_CYCLE", -3: "ED_E_DANGLING", -4: "ED_E_DUP_ID",
           -5: "ED_E_TYPE", -6: "ED_E_ARITY", -7: "ED_E_FSM", -8: "ED_E_CUDA", -9: "ED_E_UNSUPPORTED",
           -10: "ED_E_WORKSPACE", -11: "ED_E_OOM"}
@@ -55,7 +56,8 @@ class ed_fsm_t(ctypes.Structure):
 
 
 class ed_plan_opts_t(ctypes.Structure):
-    _fields_ = [("layout", ctypes.c_int32), ("staging", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+    _fields_ = [("layout", ctypes.c_int32), ("staging", ctypes.c_int32), ("policy", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 _INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bound", "num_rows", "hidden", "dtype",
@@ -228,7 +230,7 @@ class LearnedFsm:
         self.table = [(tuple(f.entries[e].key[i] for i in range(f.entries[e].key_len)), f.entries[e].action)
                       for e in range(f.num_entries)]
         self.q = {}
-        key = (ctypes.c_int32 * max(num_types, 1))()
+        key = (ctypes.c_int32 * (num_types + 1))()   # E_max keys: type set + argmax type
         kl, a, v = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
         for k in range(self.info["q_entries"]):
             _check(LIB.ed_fsm_learned_q(handle, k, key, ctypes.byref(kl), ctypes.byref(a), ctypes.byref(v)))
@@ -314,7 +316,7 @@ class GraphBatch:
 
 
 def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: int = ED_ENC_SORT,
-            layout: int = ED_LAYOUT_SCHEDULE_ORDER, staging: int = 0) -> Plan:
+            layout: int = ED_LAYOUT_SCHEDULE_ORDER, staging: int = 0, policy: int = 0) -> Plan:
     """graphs: a GraphBatch, or objects with numpy fields type/in_off/in_idx/ext and int root
     (workloads.Graph); types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype.
     The C call runs without the GIL (ctypes), so several host threads can plan concurrently."""
@@ -331,7 +333,7 @@ def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: in
         keep.append(ka)
         earr[k] = ed_fsm_entry_t(len(ka), _ptr(ka), int(act))
     f = ed_fsm_t(encoder, len(fsm), earr, 0)
-    opts = ed_plan_opts_t(layout, staging, (ctypes.c_int32 * 6)())
+    opts = ed_plan_opts_t(layout, staging, policy, (ctypes.c_int32 * 5)())
     h = ctypes.c_void_p()
     _check(LIB.ed_plan(garr, ngraphs, tarr, len(types), ctypes.byref(f), ctypes.byref(opts), ctypes.byref(h)))
     return Plan(h, len(types))

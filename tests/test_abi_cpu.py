@@ -304,3 +304,24 @@ def test_execute_checks_token_ids_and_weight_pointers():
     max_w = max(-1 - int(x) for g in fc.graphs for x in g.in_idx if x < 0 and x != -(2 ** 31))
     assert _execute_host_checks(pfc, [_dummy_set(max_w + 1)] + [_dummy_set()] * (len(fc.types) - 1)) == _CODE["ED_E_CUDA"]
     assert _execute_host_checks(pfc, [_dummy_set(max_w)] + [_dummy_set()] * (len(fc.types) - 1)) == _CODE["ED_E_INVALID_ARG"]
+
+
+@pytest.mark.parametrize("policy", ["depth", "agenda", "sc"])
+def test_comparator_policies_bit_exact_with_oracle(policy):
+    """The Fig. 8 comparators (P:107 depth / agenda, P:436 sufficient condition) in ed_plan equal the
+    oracle's schedulers batch for batch, on the Fig. 1 fixture and on random minibatches of every
+    workload family."""
+    pol = {"depth": E.ED_POLICY_DEPTH, "agenda": E.ED_POLICY_AGENDA, "sc": E.ED_POLICY_SC}[policy]
+
+    def ref(m):
+        if policy == "depth":
+            return S.depth_schedule(m)
+        return S.run_alg1(m, S.agenda_chooser(m) if policy == "agenda" else S.sc_chooser())
+    g, names = W.fig1_fixture()
+    plan = E.ed_plan([g], _fixture_types(names), [], policy=pol)
+    assert [(t, sorted(b)) for t, b in plan.schedule()] == ref(Merged([g], 3))
+    for wl in (W.treelstm(6, (2, 9), 32, "fp32", cfg=5), W.bilstm(5, (2, 8), 32, "fp32", cfg=6),
+               W.lattice(4, (3, 10), 32, "fp32", cfg=7), W.treelstm_2type(6, (2, 9), 32, "fp32", cfg=8)):
+        plan = E.ed_plan(wl.graphs, wl.types, [], policy=pol)
+        m = Merged(wl.graphs, len(wl.types))
+        assert [(t, sorted(b)) for t, b in plan.schedule()] == ref(m), wl.name

@@ -141,7 +141,14 @@ CASES = [
     ("lattice_base", lambda: W.lattice(8, (6, 12), 32, "fp32"), dict(encoder="base", max_episodes=120,
                                                                       check_every=30)),
     ("treelstm_2type", lambda: W.treelstm_2type(10, (3, 14), 32, "fp32", cfg=7), dict(max_episodes=200)),
+    ("lattice_max", lambda: W.lattice(8, (6, 12), 32, "fp32"), dict(encoder="max", max_episodes=120, check_every=30)),
+    ("trees_max", lambda: trees(), dict(encoder="max", max_episodes=150)),
 ]
+
+
+def _flat(key, encoder):
+    """Oracle key -> C ABI key: an E_max state (set, argmax) is the set followed by the argmax type."""
+    return tuple(key[0]) + (key[1],) if encoder == "max" else tuple(key)
 
 
 @pytest.mark.parametrize("name,make,kw", CASES, ids=[c[0] for c in CASES])
@@ -150,7 +157,7 @@ def test_c_learner_bit_exact_with_oracle(name, make, kw):
     wl = make()
     cfg = RLConfig(**kw)
     ref = train(instances(wl), cfg)
-    enc = E.ED_ENC_BASE if cfg.encoder == "base" else E.ED_ENC_SORT
+    enc = {"base": E.ED_ENC_BASE, "max": E.ED_ENC_MAX}.get(cfg.encoder, E.ED_ENC_SORT)
     got = E.ed_fsm_learn(wl.graphs, wl.types, encoder=enc, alpha=cfg.alpha, lr=cfg.lr, eps0=cfg.eps0,
                          eps_decay=cfg.eps_decay, eps_every=cfg.eps_every, eps_floor=cfg.eps_floor,
                          n_steps=cfg.n_steps, max_episodes=cfg.max_episodes, check_every=cfg.check_every,
@@ -158,8 +165,12 @@ def test_c_learner_bit_exact_with_oracle(name, make, kw):
     assert got.info["episodes"] == ref.episodes
     assert got.checkpoints == ref.checkpoints
     assert got.info["lower_bound"] == ref.lower_bound
-    assert dict(got.table) == ref.table
-    assert got.q == ref.q                                    # exact: same arithmetic in the same order
+    assert dict(got.table) == {_flat(k, cfg.encoder): a for k, a in ref.table.items()}
+    assert got.q == {(_flat(k, cfg.encoder), a): v for (k, a), v in ref.q.items()}   # exact: same order
+    if cfg.encoder == "max":   # the E_max table drives ed_plan exactly as the oracle's Alg. 1
+        plan = E.ed_plan(wl.graphs, wl.types, got.table, encoder=E.ED_ENC_MAX)
+        m = Merged(wl.graphs, len(wl.types))
+        assert [(t, sorted(mem)) for t, mem in plan.schedule()] == fsm_schedule(m, ref.table, "max")
 
 
 def test_learned_table_drives_ed_plan():
