@@ -302,6 +302,7 @@ def main():
     ap.add_argument("--layout", default="schedule", choices=["schedule", "pq"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--staging", default="auto", choices=["auto", "off"])
+    ap.add_argument("--step-order", default="level", choices=["level", "schedule"])
     ap.add_argument("--fsm", default="learned", choices=["learned", "learned_instance", "priority"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
@@ -337,7 +338,8 @@ def main():
     else:
         fsm = E.fsm_from_priority(wl.priority, len(wl.types))
     staging = E.ED_STAGING_OFF if args.staging == "off" else E.ED_STAGING_AUTO
-    plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging)
+    step_order = E.ED_ORDER_SCHEDULE if args.step_order == "schedule" else E.ED_ORDER_LEVEL
+    plan = E.ed_plan(wl.graphs, wl.types, fsm, layout=layout, staging=staging, step_order=step_order)
     weights = E.DeviceWeights(wl.types, wl.params)
     ws = E.Workspace(plan)
     tdt = torch.bfloat16 if wl.dtype == "bf16" else torch.float32
@@ -395,7 +397,7 @@ def main():
     host_out = [torch.empty(res_shape, dtype=out.dtype, pin_memory=True) for _ in range(2)]
     batch = E.GraphBatch(wl.graphs)
     workers = max(1, min(8, (os.cpu_count() or 1) - 1))
-    pipe = E.PlanPipeline(wl.types, fsm, workers, layout=layout, staging=staging)
+    pipe = E.PlanPipeline(wl.types, fsm, workers, layout=layout, staging=staging, step_order=step_order)
     h2d = d2h = 0
 
     def e2e_run(nsteps):
@@ -442,6 +444,17 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         meas = [x / 1e9 for x in step_ns]
         t_floor = latency_floor_us(E, wl) if world == 1 or rank == 0 else None
+        # device steps -> schedule batches (the kernel walks the batches in dependency-level order,
+        # a two-contraction cell has two device steps): t_meas per batch, listed in kernel order
+        sched = plan.schedule()
+        meas_b = [0.0] * len(sched)
+        order = []
+        for k, b in enumerate(plan.step_batches()):
+            meas_b[b] += meas[k]
+            if not order or order[-1] != b:
+                order.append(int(b))
+        steps_out = [{"batch": b, "type": wl.types[sched[b][0]].name, "m": len(sched[b][1]),
+                      "t_roof_us": round(1e6 * troof[b], 3), "t_meas_us": round(1e6 * meas_b[b], 3)} for b in order]
         per_step = {"sum_t_roof_us": 1e6 * sum(troof), "sum_t_meas_us": 1e6 * sum(meas),
                     "frac": (sum(troof) / sum(meas)) if sum(meas) > 0 else None,
                     # secondary: per-step latency floor of the persistent kernel and the
@@ -449,9 +462,7 @@ def main():
                     "t_floor_us": t_floor,
                     "achievable_frac": (sum(max(1e6 * r, t_floor) for r in troof) / (1e6 * sum(meas)))
                     if (t_floor and sum(meas) > 0) else None,
-                    "steps": [{"type": wl.types[t].name, "m": len(mem), "t_roof_us": round(1e6 * r, 3),
-                               "t_meas_us": round(1e6 * s_, 3)}
-                              for (t, mem), r, s_ in zip(plan.schedule(), troof, meas)]}
+                    "steps": steps_out}
         cpu_rate, cpu_n, cpu_dt = cpu_oracle_rate(wl, args.cpu_seconds) if world == 1 or rank == 0 else (None, 0, 0)
         line = {
             "metric": METRICS[args.config], "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
@@ -459,7 +470,7 @@ def main():
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded parse-like trees, random-init weights)",
             "config": {"workload": CONFIGS[args.config], **fsm_info, "instances_per_gpu": len(wl.graphs),
                        "nodes_per_gpu": wl.num_nodes, "batches": plan.info["num_batches"],
-                       "lower_bound": plan.info["lower_bound"], "layout": args.layout,
+                       "lower_bound": plan.info["lower_bound"], "layout": args.layout, "step_order": args.step_order,
                        "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world} ({args.scaling}; LPT by node count when strong)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
                          "frac": achieved / P, "traffic": traffic,

@@ -142,12 +142,20 @@ typedef struct {
                               second term |Frontier_a(G_t)| / |Frontier(G^a_t)| (A-1),
                               ties to the larger ready count, then the lower id.
                             Depth of an op = 1 + max depth of its node inputs (raw inputs: 0). */
-  int32_t reserved[5];   /* must be 0 */
+  int32_t step_order;    /* order in which the kernel walks the batches (their member sets are the
+                            schedule's either way): ED_ORDER_LEVEL (0): stable by dependency level
+                            (1 + the highest level among the batches producing a member's inputs),
+                            so independent chains (BiLSTM directions, separate lattices) interleave
+                            and overlap in the dataflow kernel; ED_ORDER_SCHEDULE (1): the schedule
+                            order.  ed_plan_get_step_batches reports the device order. */
+  int32_t reserved[4];   /* must be 0 */
 } ed_plan_opts_t;
 #define ED_POLICY_FSM    0
 #define ED_POLICY_DEPTH  1
 #define ED_POLICY_AGENDA 2
 #define ED_POLICY_SC     3
+#define ED_ORDER_LEVEL    0
+#define ED_ORDER_SCHEDULE 1
 
 typedef struct ed_plan_s ed_plan_t;  /* opaque plan handle */
 
@@ -236,6 +244,11 @@ ed_status_t ed_plan_get_layout(const ed_plan_t *plan, int32_t *row_of_node);
 
 /* Per (batch, fixed slot) flag: 1 = contiguous block read, 0 = gathered. [num_batches * 2] */
 ed_status_t ed_plan_get_slot_modes(const ed_plan_t *plan, int32_t *modes);
+
+/* batch_of_step[num_steps]: the schedule batch (index into ed_plan_get_schedule) each device step
+ * executes, in the order the kernel walks them (opts.step_order); a two-contraction cell's batch
+ * has two consecutive device steps.  Also the meaning of the trace / step-stamp indices. */
+ed_status_t ed_plan_get_step_batches(const ed_plan_t *plan, int32_t *batch_of_step);
 
 void ed_plan_destroy(ed_plan_t *plan);
 

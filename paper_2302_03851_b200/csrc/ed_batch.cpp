@@ -144,6 +144,8 @@ struct ed_plan_s {
   std::vector<int32_t> slot_modes;
   // lowering
   std::vector<ed::DevStep> steps;
+  std::vector<int32_t> step_batch;   // schedule batch of every device step
+  bool level_order = true;           // ED_ORDER_LEVEL
   std::vector<int32_t> idx;
   std::vector<int32_t> root_rows;
   std::vector<int32_t> target;  // per row: sum of ed::step_contrib over the device steps writing it
@@ -480,7 +482,27 @@ static ed_status_t lower(ed_plan_t *pl) {
   pl->op_rows = pl->staged = pl->staged_bytes = 0;
   std::vector<std::pair<int32_t, int32_t>> stage_pairs;  // (producer row, staged H row)
   const bool staging = pl->staging && pl->dtype == ED_BF16;
-  for (int b = 0; b < nb; ++b) {
+  // device order of the batches: stable by dependency level (ED_ORDER_LEVEL), else schedule order
+  std::vector<int32_t> border(nb);
+  for (int b = 0; b < nb; ++b) border[b] = b;
+  if (pl->level_order) {
+    std::vector<int32_t> batch_of(V, -1), level(nb, 0);
+    for (int b = 0; b < nb; ++b)
+      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) batch_of[pl->members[k]] = b;
+    for (int b = 0; b < nb; ++b) {
+      int32_t lv = 0;
+      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) {
+        const int32_t v = pl->members[k];
+        for (int q = pl->in_off[v]; q < pl->in_off[v + 1]; ++q)
+          if (pl->in_idx[q] >= 0) lv = std::max(lv, level[batch_of[pl->in_idx[q]]] + 1);
+      }
+      level[b] = lv;
+    }
+    std::stable_sort(border.begin(), border.end(), [&](int32_t a, int32_t c) { return level[a] < level[c]; });
+  }
+  pl->step_batch.clear();
+  for (int bi = 0; bi < nb; ++bi) {
+    const int b = border[bi];
     const int t = pl->batch_type[b];
     const ed_op_type_t &ot = pl->types[t];
     std::vector<int32_t> mem(pl->members.begin() + pl->batch_off[b], pl->members.begin() + pl->batch_off[b + 1]);
@@ -579,6 +601,7 @@ static ed_status_t lower(ed_plan_t *pl) {
       pl->idx[offs + m] = static_cast<int32_t>(pl->idx.size());
     }
     pl->steps.push_back(st);
+    pl->step_batch.push_back(b);
     // two-contraction cells: the dependent second GEMM is its own device step over the same rows
     if (ot.cell_kind == ED_CELL_LATTICE_WORD) {
       ed::DevStep s2 = st;  // l = s(W_l [x_e; c^w] + b_l): x_e = slot 1 (external char), c^w = own row
@@ -594,6 +617,7 @@ static ed_status_t lower(ed_plan_t *pl) {
       s2.arg[1] = st.out_row0;
       s2.nslots = 2;
       pl->steps.push_back(s2);
+      pl->step_batch.push_back(b);
     } else if (ot.cell_kind == ED_CELL_MVRNN_INTERNAL) {
       // step 1 (st): u = [B a; A b] (SIMT matvecs) -> U; step 2: p = tanh(W u + b) -> H, reading the
       // node's own U rows; step 3: P^T = [A^T | B^T] W_M^T -> Mx (rows m*h, K = 2h, N = h)
@@ -616,6 +640,7 @@ static ed_status_t lower(ed_plan_t *pl) {
       sp.arg[1] = 0;
       sp.nslots = 1;
       pl->steps.push_back(sp);
+      pl->step_batch.push_back(b);
       ed::DevStep sm = st;
       sm.cell = ed::kCellMvMat;
       sm.wsel = 1;
@@ -628,6 +653,7 @@ static ed_status_t lower(ed_plan_t *pl) {
       }
       sm.n_col_tiles = (h + sm.units - 1) / sm.units;
       pl->steps.push_back(sm);
+      pl->step_batch.push_back(b);
     } else if (ot.cell_kind == ED_CELL_TAGGER) {
       ed::DevStep s2 = st;  // y = W2 t + b2 with t in the node's own h row
       s2.cell = ed::kCellTaggerOut;
@@ -639,6 +665,7 @@ static ed_status_t lower(ed_plan_t *pl) {
       s2.arg[0] = st.out_row0;
       s2.nslots = 1;
       pl->steps.push_back(s2);
+      pl->step_batch.push_back(b);
     }
   }
   // instance outputs: the epilogue producing an instance's root row also stores it into
@@ -850,8 +877,10 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   const int layout = opts ? opts->layout : ED_LAYOUT_SCHEDULE_ORDER;
   if (layout != ED_LAYOUT_SCHEDULE_ORDER && layout != ED_LAYOUT_PQ) return fail(ED_E_INVALID_ARG, "unknown layout");
   if (opts)
-    for (int k = 0; k < 5; ++k)
+    for (int k = 0; k < 4; ++k)
       if (opts->reserved[k] != 0) return fail(ED_E_INVALID_ARG, "opts.reserved must be 0");
+  if (opts && opts->step_order != ED_ORDER_LEVEL && opts->step_order != ED_ORDER_SCHEDULE)
+    return fail(ED_E_INVALID_ARG, "unknown step order");
   if (opts && (opts->policy < ED_POLICY_FSM || opts->policy > ED_POLICY_SC))
     return fail(ED_E_INVALID_ARG, "unknown batching policy");
   if (opts && opts->staging != ED_STAGING_AUTO && opts->staging != ED_STAGING_OFF)
@@ -860,6 +889,7 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
   if (!pl) return fail(ED_E_OOM, "out of host memory");
   pl->types.assign(types, types + num_types);
   pl->staging = !(opts && opts->staging == ED_STAGING_OFF);
+  pl->level_order = !(opts && opts->step_order == ED_ORDER_SCHEDULE);
   pl->hidden = types[0].hidden;
   pl->dtype = types[0].dtype;
   for (int t = 0; t < num_types; ++t) {
@@ -983,6 +1013,12 @@ ed_status_t ed_plan_get_layout(const ed_plan_t *pl, int32_t *row) {
 ed_status_t ed_plan_get_slot_modes(const ed_plan_t *pl, int32_t *modes) {
   if (!pl || !modes) return fail(ED_E_INVALID_ARG, "null argument");
   std::copy(pl->slot_modes.begin(), pl->slot_modes.end(), modes);
+  return ED_OK;
+}
+
+ed_status_t ed_plan_get_step_batches(const ed_plan_t *pl, int32_t *out) {
+  if (!pl || !out) return fail(ED_E_INVALID_ARG, "null argument");
+  std::copy(pl->step_batch.begin(), pl->step_batch.end(), out);
   return ED_OK;
 }
 

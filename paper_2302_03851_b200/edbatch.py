@@ -24,6 +24,7 @@ ED_RL_EPISODE_INSTANCE, ED_RL_EPISODE_MERGED = 0, 1
 ED_LAYOUT_SCHEDULE_ORDER, ED_LAYOUT_PQ = 0, 1
 ED_STAGING_AUTO, ED_STAGING_OFF = 0, 1
 ED_POLICY_FSM, ED_POLICY_DEPTH, ED_POLICY_AGENDA, ED_POLICY_SC = 0, 1, 2, 3
+ED_ORDER_LEVEL, ED_ORDER_SCHEDULE = 0, 1
 STATUS = {0: "ED_OK", -1: "ED_E_INVALID_ARG", -2: "ED_E_CYCLE", -3: "ED_E_DANGLING", -4: "ED_E_DUP_ID",
           -5: "ED_E_TYPE", -6: "ED_E_ARITY", -7: "ED_E_FSM", -8: "ED_E_CUDA", -9: "ED_E_UNSUPPORTED",
           -10: "ED_E_WORKSPACE", -11: "ED_E_OOM"}
@@ -57,7 +58,7 @@ class ed_fsm_t(ctypes.Structure):
 
 class ed_plan_opts_t(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("staging", ctypes.c_int32), ("policy", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("step_order", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 _INFO_I64 = ("num_nodes", "num_instances", "num_batches", "num_steps", "lower_bound", "num_rows", "hidden", "dtype",
@@ -116,6 +117,7 @@ def _load() -> ctypes.CDLL:
     lib.ed_plan_get_schedule.argtypes = [ctypes.c_void_p, _i32p, _i32p, _i32p]
     lib.ed_plan_get_layout.argtypes = [ctypes.c_void_p, _i32p]
     lib.ed_plan_get_slot_modes.argtypes = [ctypes.c_void_p, _i32p]
+    lib.ed_plan_get_step_batches.argtypes = [ctypes.c_void_p, _i32p]
     lib.ed_plan_destroy.argtypes = [ctypes.c_void_p]
     lib.ed_plan_destroy.restype = None
     lib.ed_packed_bytes.argtypes = [ctypes.c_int32] * 5
@@ -143,6 +145,7 @@ def _load() -> ctypes.CDLL:
     lib.ed_last_error.restype = ctypes.c_char_p
     lib.ed_version.restype = ctypes.c_char_p
     for f in ("ed_plan", "ed_plan_info", "ed_plan_get_schedule", "ed_plan_get_layout", "ed_plan_get_slot_modes",
+              "ed_plan_get_step_batches",
               "ed_pack_weights", "ed_execute", "ed_execute_launch_count"):
         getattr(lib, f).restype = ctypes.c_int32
     return lib
@@ -295,6 +298,12 @@ class Plan:
         _check(LIB.ed_plan_get_slot_modes(self.handle, _ptr(m)))
         return m[:2 * self.info["num_batches"]].reshape(-1, 2)
 
+    def step_batches(self) -> np.ndarray:
+        """Schedule batch of every device step, in kernel order (ed_plan_get_step_batches)."""
+        sb = np.zeros(max(self.info["num_steps"], 1), np.int32)
+        _check(LIB.ed_plan_get_step_batches(self.handle, _ptr(sb)))
+        return sb[:self.info["num_steps"]]
+
     @property
     def upload_bytes(self) -> int:
         return int(LIB.ed_plan_upload_bytes(self.handle))
@@ -316,7 +325,8 @@ class GraphBatch:
 
 
 def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: int = ED_ENC_SORT,
-            layout: int = ED_LAYOUT_SCHEDULE_ORDER, staging: int = 0, policy: int = 0) -> Plan:
+            layout: int = ED_LAYOUT_SCHEDULE_ORDER, staging: int = 0, policy: int = 0,
+            step_order: int = 0) -> Plan:
     """graphs: a GraphBatch, or objects with numpy fields type/in_off/in_idx/ext and int root
     (workloads.Graph); types: objects with kind/num_slots/variadic/has_ext/weight_set/hidden/out_dim/dtype.
     The C call runs without the GIL (ctypes), so several host threads can plan concurrently."""
@@ -333,7 +343,7 @@ def ed_plan(graphs, types, fsm: Sequence[Tuple[Sequence[int], int]], encoder: in
         keep.append(ka)
         earr[k] = ed_fsm_entry_t(len(ka), _ptr(ka), int(act))
     f = ed_fsm_t(encoder, len(fsm), earr, 0)
-    opts = ed_plan_opts_t(layout, staging, policy, (ctypes.c_int32 * 5)())
+    opts = ed_plan_opts_t(layout, staging, policy, step_order, (ctypes.c_int32 * 4)())
     h = ctypes.c_void_p()
     _check(LIB.ed_plan(garr, ngraphs, tarr, len(types), ctypes.byref(f), ctypes.byref(opts), ctypes.byref(h)))
     return Plan(h, len(types))
