@@ -31,7 +31,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
 }
 
 __global__ void __launch_bounds__(128, 1) probe(int variant, int npass, __nv_bfloat16 *H, float *C, const float *Cin,
-                                                long long *out) {
+                                                long long *out, int one_warp) {
   __shared__ uint32_t tslot;
   __shared__ float sbias[5 * 512];
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128, 1) probe(int variant, int npass, __nv_bfl
   const float4 *clp = reinterpret_cast<const float4 *>(Cin + (size_t)row * h);
   const float4 c0 = clp[0], c1 = clp[1];  // child c: loaded before the timed passes (as prefetched)
   keep += c0.x;
-  for (int sp = 0; sp < npass; ++sp) {
+  for (int sp = 0; sp < (one_warp && warp > 0 ? 0 : npass); ++sp) {
     const long long t0 = clock64();
     const int j0 = (sp % 6) * 8;
     float z[5][8];
@@ -133,12 +133,13 @@ int main() {
   cudaMalloc(&out, sizeof(hout));
   const char *names[] = {"full pass", "no stores", "no MUFU", "stores+math, no TMEM", "f16x2 tanh",
                          "bias+FMA only", "TMEM ld only"};
+  for (int ow = 0; ow < 2; ++ow)
   for (int v = 0; v < 7; ++v) {
-    for (int rep = 0; rep < 2; ++rep) probe<<<grid, 128>>>(v, 12, H, C, Cin, out);
+    for (int rep = 0; rep < 2; ++rep) probe<<<grid, 128>>>(v, 12, H, C, Cin, out, ow);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("%s: %s\n", names[v], cudaGetErrorString(e)); return 1; }
     cudaMemcpy(hout, out, sizeof(hout), cudaMemcpyDeviceToHost);
-    printf("%-22s cycles per pass (CTA 0, passes 0..11):", names[v]);
+    printf("%s %-22s cycles per pass (CTA 0, passes 0..11):", ow ? "1 warp " : "4 warps", names[v]);
     for (int sp = 0; sp < 12; ++sp) printf(" %lld", hout[sp]);
     printf("\n");
   }
