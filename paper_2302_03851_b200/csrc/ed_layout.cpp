@@ -78,7 +78,39 @@ class PQTree {
     log_.clear();
     logged_.clear();
   }
-  void commit() { in_txn_ = false; log_.clear(); logged_.clear(); }
+  // A committed transaction that changed the tree stamps every node it modified or created with a
+  // new epoch: a batch whose operand subtrees carry no stamp newer than its last processing cannot
+  // derive new broadcast constraints (A-10: such a batch may be skipped, results are identical).
+  void commit() {
+    if (changed_since_begin()) {
+      ++epoch_;
+      stamp_.resize(nodes_.size(), 0);
+      for (const auto &e : log_) stamp_[e.first] = epoch_;
+      for (size_t id = saved_size_; id < nodes_.size(); ++id) stamp_[id] = epoch_;
+    }
+    in_txn_ = false;
+    log_.clear();
+    logged_.clear();
+  }
+  uint32_t epoch() const { return epoch_; }
+  // newest stamp in the subtree of r (children f..l only when r is a partial Q run)
+  uint32_t subtree_stamp(int r, int f, int l) const {
+    uint32_t m = stamp_of(r);
+    std::vector<int> st;
+    const auto &ch = nodes_[r].ch;
+    if (nodes_[r].kind == QN) {
+      for (int k = f; k <= l; ++k) st.push_back(ch[k]);
+    } else {
+      st.assign(ch.begin(), ch.end());
+    }
+    while (!st.empty()) {
+      const int x = st.back();
+      st.pop_back();
+      m = std::max(m, stamp_of(x));
+      for (int c : nodes_[x].ch) st.push_back(c);
+    }
+    return m;
+  }
   void rollback() {
     for (auto it = log_.rbegin(); it != log_.rend(); ++it) nodes_[it->first] = it->second;
     nodes_.resize(saved_size_);
@@ -192,6 +224,9 @@ class PQTree {
   int saved_root_ = -1;
   std::vector<std::pair<int, Node>> log_;
   std::vector<char> logged_;
+  std::vector<uint32_t> stamp_;
+  uint32_t epoch_ = 0;
+  uint32_t stamp_of(int id) const { return id < static_cast<int>(stamp_.size()) ? stamp_[id] : 0; }
 
   void touch(int id) {
     if (!in_txn_ || id >= static_cast<int>(saved_size_)) return;
@@ -557,7 +592,11 @@ std::vector<int32_t> plan_layout_pq(const LayoutInput &in) {
   }
   double t1 = now();
   int sweeps = 0;
-  // BroadcastConstraint: sweeps until no batch changes the tree
+  double t_derive = 0, t_reduce = 0;
+  // BroadcastConstraint: sweeps until no batch changes the tree.  A batch whose operand subtrees
+  // are unchanged since its last processing is skipped (A-10: its constraints are already applied).
+  std::vector<int64_t> done_epoch(nb, -1);
+  int64_t skipped = 0;
   for (int sweep = 0; sweep < 200; ++sweep) {
     ++sweeps;
     bool any = false;
@@ -565,6 +604,19 @@ std::vector<int32_t> plan_layout_pq(const LayoutInput &in) {
       if (!alive[b] || ops[b].size() < 2) continue;
       const int m = static_cast<int>(ops[b][0].size());
       if (m < 2) continue;
+      if (done_epoch[b] >= 0) {
+        uint32_t newest = 0;
+        for (const auto &O : ops[b]) {
+          int r, f, l;
+          T.min_subtree(O, &r, &f, &l);
+          newest = std::max(newest, T.subtree_stamp(r, f, l));
+        }
+        if (static_cast<int64_t>(newest) <= done_epoch[b]) {
+          ++skipped;
+          continue;
+        }
+      }
+      const double td0 = dbg ? now() : 0;
       // position of each variable in each operand
       std::vector<std::vector<int>> cons;  // position sets
       for (size_t o = 0; o < ops[b].size(); ++o) {
@@ -615,6 +667,8 @@ std::vector<int32_t> plan_layout_pq(const LayoutInput &in) {
       }
       std::sort(cons.begin(), cons.end());
       cons.erase(std::unique(cons.begin(), cons.end()), cons.end());
+      const double td1 = dbg ? now() : 0;
+      t_derive += td1 - td0;
       T.begin();
       bool ok = true;
       for (const auto &ps : cons) {
@@ -625,6 +679,7 @@ std::vector<int32_t> plan_layout_pq(const LayoutInput &in) {
         }
         if (!ok) break;
       }
+      if (dbg) t_reduce += now() - td1;
       if (!ok) {
         T.rollback();
         alive[b] = 0;
@@ -632,6 +687,7 @@ std::vector<int32_t> plan_layout_pq(const LayoutInput &in) {
       } else {
         if (T.changed_since_begin()) any = true;
         T.commit();
+        done_epoch[b] = T.epoch();
       }
       if (dbg) if (const char *e = T.check()) std::fprintf(stderr, "[pq] sweep %d batch %d (%s): %s\n", sweep, b, ok ? "ok" : "rolled back", e);
     }
@@ -763,6 +819,8 @@ std::vector<int32_t> plan_layout_pq(const LayoutInput &in) {
   if (dbg) {
     int nalive = 0;
     for (int b = 0; b < nb; ++b) nalive += alive[b] && ops[b].size() > 1;
+    std::fprintf(stderr, "[pq] broadcast: derive %.1f ms, reduce %.1f ms, %lld batch visits skipped\n", t_derive,
+                 t_reduce, static_cast<long long>(skipped));
     std::fprintf(stderr, "[pq] construct %.1f ms, broadcast %.1f ms (%d sweeps), order %.1f ms, alive %d/%d\n", t1 - t0,
                  t2 - t1, sweeps, now() - t2, nalive, nb);
   }

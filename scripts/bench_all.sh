@@ -2,7 +2,7 @@
 # secondary bench lines: every config, both layouts (development / DESIGN.md numbers)
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
-for c in cfg3 cfg3_gru cfg3_2type cfg2 cfg5 cfg4_treefc cfg4_mvrnn cfg1; do
+for c in cfg3 cfg3_gru cfg3_2type cfg2 cfg5 cfg5_h512 cfg5_gru cfg4_treefc cfg4_mvrnn cfg1; do
   for l in ${LAYOUTS:-schedule pq}; do
     timeout -s KILL 300 python bench.py --config $c --layout $l --cpu-seconds 3 --e2e-steps 3 > gpurun_out/bench_${c}_${l}_$TAG.json 2>gpurun_out/bench_${c}_${l}_$TAG.err
     python - "$c" "$l" "gpurun_out/bench_${c}_${l}_$TAG.json" <<'PY'
