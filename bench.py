@@ -91,6 +91,16 @@ def _weak_workload(name: str, rank: int):
     raise KeyError(name)
 
 
+def host_cpu():
+    """CPU model and logical core count of this host (lscpu), for the CPU baseline."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        model = next((l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")), "?")
+    except Exception:
+        model = "?"
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -256,6 +266,44 @@ def cpu_oracle_rate(wl, seconds: float, max_instances: int = 256):
     if limiter is not None:
         limiter.unregister() if hasattr(limiter, "unregister") else None
     return n / dt, n, dt
+
+
+_WORKER_WL = None
+
+
+def _oracle_worker_init(name):
+    global _WORKER_WL
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        pass
+    _WORKER_WL = W.config(name)
+
+
+def _oracle_worker_eval(i):
+    from oracle.evaluate import evaluate_recursive
+    if i >= 0:
+        evaluate_recursive(_WORKER_WL, [i % len(_WORKER_WL.graphs)])
+    return i
+
+
+def cpu_oracle_rate_all_cores(name, rate1: float, seconds: float):
+    """The same fp64 oracle on every host core (1-thread and all-core rates): a
+    process pool over instances (spawned workers, 1 BLAS thread each), a bounded sample sized from
+    the 1-core rate.  Returns (instances/s, instances, seconds, cores)."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    n = max(cores, min(4096, int(rate1 * cores * seconds)))
+    with cf.ProcessPoolExecutor(cores, mp_context=mp.get_context("spawn"), initializer=_oracle_worker_init,
+                                initargs=(name,)) as ex:
+        list(ex.map(_oracle_worker_eval, [-1] * cores))   # workers up and holding the workload
+        t0 = time.perf_counter()
+        list(ex.map(_oracle_worker_eval, range(n), chunksize=max(1, n // (4 * cores))))
+        dt = time.perf_counter() - t0
+    return n / dt, n, dt, cores
 
 
 def run_reference(args, rank, world):
@@ -464,6 +512,12 @@ def main():
                     if (t_floor and sum(meas) > 0) else None,
                     "steps": steps_out}
         cpu_rate, cpu_n, cpu_dt = cpu_oracle_rate(wl, args.cpu_seconds) if world == 1 or rank == 0 else (None, 0, 0)
+        all_rate = all_n = all_dt = all_cores = None
+        if args.cpu_seconds >= 5 and world == 1:
+            try:
+                all_rate, all_n, all_dt, all_cores = cpu_oracle_rate_all_cores(args.config, cpu_rate, args.cpu_seconds / 2)
+            except Exception as e:  # pragma: no cover - reported, never fatal
+                all_rate = f"failed: {e}"
         line = {
             "metric": METRICS[args.config], "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -480,7 +534,9 @@ def main():
             "per_step_roofline": per_step,
             "cpu_baseline": {"value": cpu_rate, "unit": "instances/s", "cores": 1, "kind": "oracle",
                              "sample": f"{cpu_n} instances of the {args.config} minibatch in {cpu_dt:.1f} s, fp64 "
-                                       "per-node recursive oracle, 1 BLAS thread"},
+                                       "per-node recursive oracle, 1 BLAS thread",
+                             "all_cores": {"value": all_rate, "cores": all_cores, "instances": all_n,
+                                           "seconds": all_dt, "host": host_cpu()}},
             "e2e": {"value": n_inst_total / (e2e_ms / 1e3), "unit": "instances/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "includes": "per step: ed_plan (host Alg. 1 + layout + lowering, on a pool of host threads "
