@@ -532,6 +532,13 @@ def main():
                          "algorithmic_flops_per_launch": F_tot, "algorithmic_bytes_per_launch": B_tot,
                          "peak_source": f"{src} bf16_tflops (burst; kernel timed alone)"},
             "per_step_roofline": per_step,
+            # layout evidence (Table 4): what a copy-based executor (DyNet's
+            # gather / scatter kernels) would move for this plan's layout, and what the kernel reads as
+            # contiguous / staged blocks instead of row gathers
+            "layout": {"layout": args.layout, "copy_bytes": plan.info["copy_bytes"],
+                       "copy_kernels": plan.info["copy_kernels"], "contig_operands": plan.info["contig_operands"],
+                       "gather_operands": plan.info["gather_operands"], "staged_operands": plan.info["staged_operands"],
+                       "staged_bytes": plan.info["staged_bytes"], "layout_ms": round(plan.info["layout_us"] / 1e3, 2)},
             "cpu_baseline": {"value": cpu_rate, "unit": "instances/s", "cores": 1, "kind": "oracle",
                              "sample": f"{cpu_n} instances of the {args.config} minibatch in {cpu_dt:.1f} s, fp64 "
                                        "per-node recursive oracle, 1 BLAS thread",

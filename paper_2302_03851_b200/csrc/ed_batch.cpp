@@ -529,6 +529,18 @@ static ed_status_t lower(ed_plan_t *pl) {
       const int umax = st.units;
       for (int u = umax; u >= 16; u -= 16)
         if (mt * ((h + u - 1) / u) <= 148) st.units = u;
+      // development override for batches that do not fit one wave: ED_UNITS="cell:units,..."
+      // (scripts/units_sweep.sh)
+      static const char *ov = std::getenv("ED_UNITS");
+      if (ov && mt * ((h + st.units - 1) / st.units) > 148) {
+        for (const char *q = ov; *q;) {
+          int c = 0, u = 0, n = 0;
+          if (std::sscanf(q, "%d:%d%n", &c, &u, &n) != 2) break;
+          if (c == ot.cell_kind && u >= 16 && u <= umax && u % 16 == 0) st.units = u;
+          q += n;
+          if (*q == ',') ++q;
+        }
+      }
     }
     st.n_col_tiles = st.units > 0 ? (h + st.units - 1) / st.units : 0;
     if (ot.cell_kind == ED_CELL_LINEAR_OUT && pl->dtype == ED_BF16) {

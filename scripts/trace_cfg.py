@@ -39,3 +39,17 @@ it = [(c, int(pc[c, 1] - base), int(pc[c, 0] - base), int(pc[c, 3] - base) if pc
 it.sort(key=lambda r: -r[4])
 print("per CTA (cta, synced, item1 done, item2 done, all done) slowest first:", it[:16])
 print("fastest:", it[-6:])
+
+# first step (device step 0): per-CTA item completion times (slots 0..2) and item count (slot 3)
+print("step 0 per-CTA item ends (us after kernel start), by number of items:")
+t0k = int(ts[0])
+by = {}
+for c in range(148):
+    n = int(pc[c, 3])
+    if n <= 0 or n > 3:
+        continue
+    ends = [round((int(pc[c, k]) - t0k) / 1e3, 1) for k in range(min(n, 3))]
+    by.setdefault(n, []).append(ends)
+for n, rows in sorted(by.items()):
+    arr = np.array(rows)
+    print(f"  {n} items: {len(rows)} CTAs; item-end medians {np.median(arr, axis=0).tolist()}; max last {arr[:, -1].max()}")
