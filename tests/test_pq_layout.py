@@ -298,3 +298,28 @@ def test_pq_layout_avoids_copies_of_the_label_layout(wlf):
     _, sched_kernels = OL.copy_bytes(m, so, OL.schedule_order_layout(m, so), 64)
     assert pq_bytes < label_bytes and pq_kernels < label_kernels
     assert pq_kernels <= sched_kernels
+
+
+def test_static_subgraph_ablation_pq_leaves_only_broadcasts():
+    """Table 4 / P:438: on the cells' static subgraphs the PQ layout removes every gather / scatter
+    except broadcasts (x read by every gate) -- the "ideal memory allocation order" -- and needs far
+    fewer copy kernels and bytes than the label layout.  Reading S-2 decompositions (script)."""
+    import importlib.util
+    path = os.path.join(os.path.dirname(os.path.dirname(__file__)), "scripts", "static_subgraph_ablation.py")
+    spec = importlib.util.spec_from_file_location("ssa", path)
+    ssa = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ssa)
+    types = [W.OpType(k, ssa.KINDS[k][0], ssa.KINDS[k][1], weight_set=i, hidden=ssa.H,
+                      has_ext=1 if ssa.KINDS[k][1] == 0 else 0, out_dim=1 if ssa.KINDS[k][0] == "linear_out" else 0,
+                      dtype="fp32") for i, k in enumerate(ssa.ORDER)]
+    for name in ("LSTMCell", "GRUCell", "TreeLSTM-Internal", "TreeLSTM-Leaf", "TreeGRU-Leaf"):
+        s = ssa.build(name)
+        ext = [v if ssa.KINDS[s.kind[v]][1] == 0 else -1 for v in range(len(s.kind))]
+        g = W.graph_from_lists([ssa.ORDER.index(k) for k in s.kind], s.ins, ext, root=len(s.kind) - 1)
+        pq = E.ed_plan([g], types, [], policy=E.ED_POLICY_AGENDA, layout=E.ED_LAYOUT_PQ)
+        sched = pq.schedule()
+        k_label, b_label = ssa.copies(sched, list(range(len(s.kind))), s)
+        k_pq, b_pq = ssa.copies(sched, list(pq.layout()), s)
+        k_bc, b_bc = ssa.copies(sched, list(pq.layout()), s, broadcasts_only=True)
+        assert (k_pq, b_pq) == (k_bc, b_bc), name          # only broadcasts remain
+        assert k_pq < k_label and 20 * b_pq < b_label, name
