@@ -355,6 +355,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--plan-threads", type=int, default=14, help="host threads planning minibatches ahead (e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -444,7 +445,7 @@ def main():
     res_shape = (wl.n_total, wl.hidden) if rg else tuple(out.shape)
     host_out = [torch.empty(res_shape, dtype=out.dtype, pin_memory=True) for _ in range(2)]
     batch = E.GraphBatch(wl.graphs)
-    workers = max(1, min(8, (os.cpu_count() or 1) - 1))
+    workers = max(1, min(args.plan_threads, (os.cpu_count() or 1) - 2))
     pipe = E.PlanPipeline(wl.types, fsm, workers, layout=layout, staging=staging, step_order=step_order)
     h2d = d2h = 0
 
