@@ -190,6 +190,12 @@ static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, i
     total += g.num_nodes;
   }
   if (total >= (int64_t(1) << 30)) return fail(ED_E_INVALID_ARG, "too many nodes");
+  {
+    int64_t edges = 0;
+    for (int gi = 0; gi < ng; ++gi)
+      if (graphs[gi].num_nodes > 0) edges += std::max<int64_t>(0, graphs[gi].in_off[graphs[gi].num_nodes]);
+    pl->in_idx.reserve(static_cast<size_t>(edges));
+  }
   pl->V = total;
   pl->ninst = ng;
   pl->gtype.resize(total);
@@ -295,7 +301,28 @@ static ed_status_t validate_and_merge(ed_plan_t *pl, const ed_graph_t *graphs, i
 // ------------------------------------------------------------------------------------------------
 // Alg. 1 with E_sort / E_base + table lookup; fallback key[0] (A-3)
 // ------------------------------------------------------------------------------------------------
+// Ascending sort of node ids (< 2^30): LSD radix (3 x 10-bit digits) for large batches, std::sort
+// for small ones.
+static void sort_ids(std::vector<int32_t> *v, std::vector<int32_t> *tmp) {
+  const size_t n = v->size();
+  if (n < 2048) {
+    std::sort(v->begin(), v->end());
+    return;
+  }
+  tmp->resize(n);
+  int32_t *a = v->data(), *b = tmp->data();
+  for (int shift = 0; shift < 30; shift += 10) {
+    uint32_t cnt[1025] = {0};
+    for (size_t i = 0; i < n; ++i) ++cnt[((static_cast<uint32_t>(a[i]) >> shift) & 1023u) + 1];
+    for (int d = 0; d < 1024; ++d) cnt[d + 1] += cnt[d];
+    for (size_t i = 0; i < n; ++i) b[cnt[(static_cast<uint32_t>(a[i]) >> shift) & 1023u]++] = a[i];
+    std::swap(a, b);
+  }
+  if (a != v->data()) std::copy(a, a + n, v->data());
+}
+
 static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm, int policy) {
+  std::vector<int32_t> sort_tmp;
   const int nt = static_cast<int>(pl->types.size());
   const int64_t V = pl->V;
   // comparators: topological depth (1 + max over node inputs; raw inputs 0)
@@ -410,7 +437,7 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm, int policy) {
     if (act < 0 || ready[act].empty()) act = skey[0];
     std::vector<int32_t> batch;
     batch.swap(ready[act]);
-    std::sort(batch.begin(), batch.end());
+    sort_ids(&batch, &sort_tmp);
     for (int32_t v : batch) {
       pl->members.push_back(v);
       for (int k = coff[v]; k < coff[v + 1]; ++k) {
@@ -505,10 +532,21 @@ static ed_status_t lower(ed_plan_t *pl) {
     const int b = border[bi];
     const int t = pl->batch_type[b];
     const ed_op_type_t &ot = pl->types[t];
-    std::vector<int32_t> mem(pl->members.begin() + pl->batch_off[b], pl->members.begin() + pl->batch_off[b + 1]);
-    std::sort(mem.begin(), mem.end(), [&](int32_t a, int32_t c) { return pl->row_of_node[a] < pl->row_of_node[c]; });
+    // members in result-row order: a batch's rows are one block (A-9), so each member goes to
+    // position row - min row directly (no comparison sort); a non-block result fails below
+    const int m = pl->batch_off[b + 1] - pl->batch_off[b];
+    std::vector<int32_t> mem(m, -1);
+    {
+      int32_t rmin = INT32_MAX;
+      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) rmin = std::min(rmin, pl->row_of_node[pl->members[k]]);
+      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) {
+        const int32_t v = pl->members[k], pos = pl->row_of_node[v] - rmin;
+        if (pos < 0 || pos >= m || mem[pos] != -1)
+          return fail(ED_E_INVALID_ARG, "internal: result operand of batch " + std::to_string(b) + " not contiguous");
+        mem[pos] = v;
+      }
+    }
     std::copy(mem.begin(), mem.end(), pl->members.begin() + pl->batch_off[b]);
-    const int m = static_cast<int>(mem.size());
     ed::DevStep st{};
     st.cell = ot.cell_kind;
     st.m = m;
@@ -945,18 +983,30 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
     const int nbat = static_cast<int>(pl->batch_type.size());
     for (int b = 0; b < nbat; ++b)
       for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) bidx[pl->members[k]] = b;
+    // (members of a batch are ascending by id, so a stable counting sort by the latest producing
+    // batch gives the (latest batch, id) order without a comparison sort)
     int32_t r = 0;
+    std::vector<int32_t> last, cnt;
     for (int b = 0; b < nbat; ++b) {
-      std::vector<std::pair<int32_t, int32_t>> key;
-      for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) {
+      const int k0 = pl->batch_off[b], k1 = pl->batch_off[b + 1];
+      last.resize(k1 - k0);
+      cnt.assign(b + 2, 0);
+      for (int k = k0; k < k1; ++k) {
         const int32_t v = pl->members[k];
-        int32_t last = -1;
+        int32_t l = -1;
         for (int q = pl->in_off[v]; q < pl->in_off[v + 1]; ++q)
-          if (pl->in_idx[q] >= 0) last = std::max(last, bidx[pl->in_idx[q]]);
-        key.emplace_back(last, v);
+          if (pl->in_idx[q] >= 0) l = std::max(l, bidx[pl->in_idx[q]]);
+        last[k - k0] = l;
+        ++cnt[l + 1];
       }
-      std::sort(key.begin(), key.end());
-      for (const auto &kv : key) pl->row_of_node[kv.second] = r++;
+      int32_t run = r;
+      for (int c = 0; c < b + 2; ++c) {
+        const int32_t n = cnt[c];
+        cnt[c] = run;
+        run += n;
+      }
+      for (int k = k0; k < k1; ++k) pl->row_of_node[pl->members[k]] = cnt[last[k - k0] + 1]++;
+      r = run;
     }
   }
   const double t3 = now_us();
