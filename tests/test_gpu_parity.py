@@ -251,3 +251,27 @@ def test_out_root_is_validated():
         E.ed_execute(plan, w, ws, out.float())
     with pytest.raises(ValueError):
         E.ed_execute(plan, w, ws, out[:2])
+
+
+@pytest.mark.parametrize("h", [1024, 768, 320])
+def test_treelstm_bf16_large_and_odd_hidden(h):
+    """Hidden sizes past the bench's: h = 1024 (K = 2048, the bias no longer fits the shared-memory
+    staging and is read from global), h = 768 and 320 (column tiles that do not divide h)."""
+    _check(W.treelstm(12, (1, 24), h, "bf16", cfg=80 + h))
+
+
+def test_lattice_h512_and_bilstm_h512():
+    _check(W.lattice(16, (1, 30), 512, "bf16", cfg=84))
+    _check(W.bilstm(10, (1, 20), 512, "bf16", cfg=85))
+
+
+def test_minibatch_of_only_external_roots_and_one_op():
+    """Degenerate minibatches: TreeFC instances that are single words (no op; the output is the input
+    row) mixed with one one-op instance, and a minibatch with no op at all."""
+    wl = W.treefc(1, (2, 2), 64, "bf16", cfg=86)
+    words = [W.Graph(np.zeros(0, np.int32), np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32), -1 - k)
+             for k in (3, 9, 17)]
+    wl.graphs = words + wl.graphs
+    _check(wl)
+    wl.graphs = words
+    _check(wl)
