@@ -368,11 +368,19 @@ def main():
         return
 
     import torch
+    # ED_BENCH_ONE_GPU=1 (test hook): every rank on cuda:0 over gloo, to exercise the N > 1 code path
+    # (sharding, RootGather, max-over-ranks timing) on a one-GPU box; never used for reported numbers
+    one_gpu = os.environ.get("ED_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2302_03851_b200 import edbatch as E
     from paper_2302_03851_b200.sharding import RootGather
 
@@ -521,7 +529,7 @@ def main():
                 all_rate = f"failed: {e}"
         line = {
             "metric": METRICS[args.config], "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded parse-like trees, random-init weights)",
             "config": {"workload": CONFIGS[args.config], **fsm_info, "instances_per_gpu": len(wl.graphs),
                        "nodes_per_gpu": wl.num_nodes, "batches": plan.info["num_batches"],
