@@ -14,9 +14,9 @@ from paper_2302_03851_b200 import edbatch as E
 cell = sys.argv[1] if len(sys.argv) > 1 else "treelstm"
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 rows = []
-for n in (1, 8, 32, 64, 128, 256, 512, 1024):
+for n in (1, 8, 32, 64, 128, 256, 512, 1024, 2048, 4096):
     wl = W.treelstm(n, (5, 40), 512, "bf16", 3, cell=cell)
-    learned = E.ed_fsm_learn(wl.graphs, wl.types)
+    learned = E.ed_fsm_learn(wl.graphs, wl.types, merged=True)
     plan = E.ed_plan(wl.graphs, wl.types, learned.table)
     w = E.DeviceWeights(wl.types, wl.params)
     ws = E.Workspace(plan)
