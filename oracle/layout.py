@@ -18,21 +18,35 @@ from .graph import Merged
 
 def schedule_order_layout(m: Merged, sched) -> List[int]:
     """ED_LAYOUT_SCHEDULE_ORDER: rows assigned batch after batch (every result operand is then one
-    contiguous block, SURVEY A-9); inside a batch, members ordered by the latest batch that
-    produces one of their node inputs (-1 if none), then by global id (reading L-1)."""
+    contiguous block, SURVEY A-9); inside a batch, members ordered by
+      1. the latest batch that produces one of their node inputs (-1 if none; reading L-1),
+      2. their earliest consumer: (consumer's batch, consumer's position inside its batch), the
+         smallest over the consumers; members without a consumer after all others (reading L-3),
+      3. global id.
+    Positions are fixed from the last batch backwards (a consumer's position is known before its
+    producers are ordered); then rows are the batches' positions offset by the earlier batches."""
     batch_of = {}
     for b, (_, members) in enumerate(sched):
         for v in members:
             batch_of[v] = b
+    consumers = m.consumers()
+    pos = {}
+    for b in range(len(sched) - 1, -1, -1):
+        members = sched[b][1]
+
+        def key(v):
+            latest = max([batch_of[u] for u in m.node_inputs(v)], default=-1)
+            earliest = min([(batch_of[w], pos[w]) for w in consumers[v]], default=(float("inf"), 0))
+            return (latest, earliest, v)
+        for k, v in enumerate(sorted(members, key=key)):
+            pos[v] = k
     row = [-1] * m.n
     r = 0
     for _, members in sched:
-        def key(v):
-            return (max([batch_of[u] for u in m.node_inputs(v)], default=-1), v)
-        for v in sorted(members, key=key):
-            row[v] = r
-            r += 1
-    assert r == m.n
+        for v in members:
+            row[v] = r + pos[v]
+        r += len(members)
+    assert r == m.n and sorted(row) == list(range(m.n))
     return row
 
 

@@ -976,37 +976,58 @@ ed_status_t ed_plan(const ed_graph_t *graphs, int32_t num_graphs, const ed_op_ty
     if (pl->row_of_node.size() != static_cast<size_t>(pl->V)) { delete pl; return fail(ED_E_UNSUPPORTED, "PQ layout planner not available"); }
   } else {
     // ED_LAYOUT_SCHEDULE_ORDER: batches in schedule order; inside a batch, members ordered by the
-    // latest batch producing one of their inputs, then by id, so that rows whose inputs are ready
-    // early share the early tiles (the dataflow kernel starts a tile when its input rows are ready)
+    // latest batch producing one of their inputs (L-1: rows whose inputs are ready early share the
+    // early tiles), then by the position of their earliest consumer (L-3: the rows one consumer tile
+    // reads come from few producer tiles, so the consumer's early tiles start while the producer
+    // step's later tiles still run), then by id.  Positions are fixed from the last batch backwards.
     pl->row_of_node.assign(pl->V, -1);
-    std::vector<int32_t> bidx(pl->V, -1);
+    std::vector<int32_t> bidx(pl->V, -1), rank(pl->V, 0);
     const int nbat = static_cast<int>(pl->batch_type.size());
     for (int b = 0; b < nbat; ++b)
       for (int k = pl->batch_off[b]; k < pl->batch_off[b + 1]; ++k) bidx[pl->members[k]] = b;
-    // (members of a batch are ascending by id, so a stable counting sort by the latest producing
-    // batch gives the (latest batch, id) order without a comparison sort)
-    int32_t r = 0;
-    std::vector<int32_t> last, cnt;
-    for (int b = 0; b < nbat; ++b) {
+    static const int l3 = std::getenv("ED_LAYOUT_L3") ? std::atoi(std::getenv("ED_LAYOUT_L3")) : 1;
+    // key = (latest producing batch + 1) * (V + 1) + (earliest consumer's global position, V if none);
+    // members are ascending by id, so a stable LSD radix sort on the key yields (key, id) order
+    std::vector<std::pair<uint64_t, int32_t>> key, tmp;
+    const uint64_t V1 = static_cast<uint64_t>(pl->V) + 1;
+    for (int b = nbat - 1; b >= 0; --b) {
       const int k0 = pl->batch_off[b], k1 = pl->batch_off[b + 1];
-      last.resize(k1 - k0);
-      cnt.assign(b + 2, 0);
+      key.clear();
+      uint64_t kmax = 0;
       for (int k = k0; k < k1; ++k) {
         const int32_t v = pl->members[k];
         int32_t l = -1;
         for (int q = pl->in_off[v]; q < pl->in_off[v + 1]; ++q)
           if (pl->in_idx[q] >= 0) l = std::max(l, bidx[pl->in_idx[q]]);
-        last[k - k0] = l;
-        ++cnt[l + 1];
+        uint64_t ck = V1 - 1;  // no consumer: after every consumed member
+        if (l3)
+          for (int q = pl->coff[v]; q < pl->coff[v + 1]; ++q) {
+            const int32_t w = pl->cons[q];
+            ck = std::min(ck, static_cast<uint64_t>(pl->batch_off[bidx[w]]) + static_cast<uint64_t>(rank[w]));
+          }
+        const uint64_t kk = static_cast<uint64_t>(l + 1) * V1 + ck;
+        kmax = std::max(kmax, kk);
+        key.emplace_back(kk, v);
       }
-      int32_t run = r;
-      for (int c = 0; c < b + 2; ++c) {
-        const int32_t n = cnt[c];
-        cnt[c] = run;
-        run += n;
+      const size_t n = key.size();
+      tmp.resize(n);
+      if (n < 1024)  // small batches: a comparison sort on (key, id) is cheaper than the histograms
+        std::sort(key.begin(), key.end());
+      else
+      for (int shift = 0; shift < 64 && (kmax >> shift) != 0; shift += 11) {
+        std::vector<uint32_t> cnt(2049, 0);
+        for (size_t i = 0; i < n; ++i) ++cnt[((key[i].first >> shift) & 2047u) + 1];
+        for (int d = 0; d < 2048; ++d) cnt[d + 1] += cnt[d];
+        for (size_t i = 0; i < n; ++i) tmp[cnt[(key[i].first >> shift) & 2047u]++] = key[i];
+        key.swap(tmp);
       }
-      for (int k = k0; k < k1; ++k) pl->row_of_node[pl->members[k]] = cnt[last[k - k0] + 1]++;
-      r = run;
+      for (size_t k = 0; k < n; ++k) rank[key[k].second] = static_cast<int32_t>(k);
+    }
+    int32_t r = 0;
+    for (int b = 0; b < nbat; ++b) {
+      const int k0 = pl->batch_off[b], k1 = pl->batch_off[b + 1];
+      for (int k = k0; k < k1; ++k) pl->row_of_node[pl->members[k]] = r + rank[pl->members[k]];
+      r += k1 - k0;
     }
   }
   const double t3 = now_us();

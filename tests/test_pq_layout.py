@@ -271,11 +271,16 @@ def test_chains_become_fully_contiguous():
 
 
 def test_pq_improves_contiguity_over_schedule_order():
-    for wl in (W.bilstm(16, (1, 30), 64, "bf16", cfg=2), W.lattice(16, (2, 30), 64, "bf16", cfg=5)):
+    """The PQ planner's objective (operands made contiguous) is at least what the schedule-order
+    layout reaches.  Since reading L-3 orders each batch by its members' consumers, the schedule-order
+    layout already makes single-direction chains contiguous (BiLSTM: equal); lattices still gain."""
+    for wl, strict in ((W.bilstm(16, (1, 30), 64, "bf16", cfg=2), False), (W.lattice(16, (2, 30), 64, "bf16", cfg=5), True)):
         pr = E.fsm_from_priority(wl.priority, len(wl.types))
         a = E.ed_plan(wl.graphs, wl.types, pr, layout=E.ED_LAYOUT_SCHEDULE_ORDER).info
         b = E.ed_plan(wl.graphs, wl.types, pr, layout=E.ED_LAYOUT_PQ).info
-        assert b["contig_operands"] > a["contig_operands"]   # the planner's objective: operands made contiguous
+        assert b["contig_operands"] >= a["contig_operands"] and b["copy_bytes"] <= a["copy_bytes"]
+        if strict:
+            assert b["contig_operands"] > a["contig_operands"]
 
 
 @pytest.mark.parametrize("wlf", [
