@@ -135,6 +135,17 @@ __device__ __forceinline__ const void *lds_ptr(const void *const *p) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)));
   return reinterpret_cast<const void *>(v);
 }
+// 256-bit global stores (sm_100): one full 32 B sector per thread
+__device__ __forceinline__ void st_v8_b32(void *a, uint4 lo, uint4 hi) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(a), "r"(lo.x), "r"(lo.y), "r"(lo.z),
+               "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_v8_f32(float *a, const float *v) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(a), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ float4 lds_f4(const float *p) {
   float4 v;
   asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(p)));
@@ -982,6 +993,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   const bool warp_live = row_tile * kTileM + (r & ~31) < st.m;
 #pragma unroll 1
   for (int sp0 = 0; sp0 < (warp_live ? nsteps : 0); sp0 += 2) {
+  uint4 hlo = make_uint4(0, 0, 0, 0);  // bf16 h of the pair's first half, stored with the second
 #pragma unroll
   for (int b2 = 0; b2 < 2; ++b2) {
     const int sp = sp0 + b2;
@@ -1117,19 +1129,24 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
         packed[k] = *reinterpret_cast<uint32_t *>(&t);
       }
       const uint4 hv4 = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      *reinterpret_cast<uint4 *>(H + orow * h + j0) = hv4;
-      if (cpy0 != nullptr) *reinterpret_cast<uint4 *>(cpy0 + j0) = hv4;
-      if (cpy1 != nullptr) *reinterpret_cast<uint4 *>(cpy1 + j0) = hv4;
-      for (int d = dbeg; d < dend; ++d) {
-        __nv_bfloat16 *dst = copy_row<__nv_bfloat16>(p, __ldg(p.idx + d));
-        if (dst != nullptr) *reinterpret_cast<uint4 *>(dst + j0) = hv4;
+      // the pair's two 8-unit halves are one 32 B run of the row: one 256-bit store per row and copy
+      // (full L2 sectors instead of two half-sector writes)
+      if (b2 == 0) {
+        hlo = hv4;
+      } else {
+        const int jp = j0 - 8;
+        st_v8_b32(H + orow * h + jp, hlo, hv4);
+        if (cpy0 != nullptr) st_v8_b32(cpy0 + jp, hlo, hv4);
+        if (cpy1 != nullptr) st_v8_b32(cpy1 + jp, hlo, hv4);
+        for (int d = dbeg; d < dend; ++d) {
+          __nv_bfloat16 *dst = copy_row<__nv_bfloat16>(p, __ldg(p.idx + d));
+          if (dst != nullptr) st_v8_b32(dst + jp, hlo, hv4);
+        }
       }
     }
     if constexpr (HAS_C) {
       float *dst = (CELL == kCellLatticeLink) ? p.X : p.C;
-      float4 *cd = reinterpret_cast<float4 *>(dst + orow * h + j0);
-      cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-      cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+      st_v8_f32(dst + orow * h + j0, cv);  // 8 fp32 = one 32 B sector
     }
     if (tr != nullptr && r == 0 && sp < 2) tr[5 + 2 * sp] = globaltimer();
   }
