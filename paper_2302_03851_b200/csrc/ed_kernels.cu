@@ -146,6 +146,17 @@ __device__ __forceinline__ void st_v8_f32(float *a, const float *v) {
                "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                : "memory");
 }
+// 256-bit L2 (.cg) loads: one full 32 B sector per thread
+__device__ __forceinline__ void ldcg_v8(const void *a, float4 &lo, float4 &hi) {
+  asm volatile("ld.global.cg.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+               : "l"(a));
+}
+__device__ __forceinline__ void ldcg_v8(const void *a, uint4 &lo, uint4 &hi) {
+  asm volatile("ld.global.cg.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+               : "l"(a));
+}
 __device__ __forceinline__ float4 lds_f4(const float *p) {
   float4 v;
   asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(p)));
@@ -979,10 +990,10 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
 #pragma unroll
   for (int b2 = 0; b2 < 2; ++b2) {
 #pragma unroll
-    for (int q = 0; q < 2 * NC; ++q) cbuf[b2][q] = __ldcg((q < 2 ? cp0 : cp1) + b2 * 2 + (q & 1));
-#pragma unroll
-    for (int q = 0; q < NH; ++q) hbuf[b2][q] = __ldcg((q == 0 ? hp0 : hp1) + b2);
+    for (int q = 0; q < NC; ++q) ldcg_v8((q == 0 ? cp0 : cp1) + b2 * 2, cbuf[b2][2 * q], cbuf[b2][2 * q + 1]);
   }
+#pragma unroll
+  for (int q = 0; q < NH; ++q) ldcg_v8(q == 0 ? hp0 : hp1, hbuf[0][q], hbuf[1][q]);  // both halves of pair 0
   mbar_wait(tfull_bar, parity);
   tc_fence_after();
   if (tr != nullptr && r == 0) *tr = globaltimer();
@@ -1006,9 +1017,11 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
     for (int q = 0; q < NH; ++q) hc[q] = hbuf[b2][q];
     if (sp + 2 < nsteps) {
 #pragma unroll
-      for (int q = 0; q < 2 * NC; ++q) cbuf[b2][q] = __ldcg((q < 2 ? cp0 : cp1) + (sp + 2) * 2 + (q & 1));
+      for (int q = 0; q < NC; ++q) ldcg_v8((q == 0 ? cp0 : cp1) + (sp + 2) * 2, cbuf[b2][2 * q], cbuf[b2][2 * q + 1]);
+      if (b2 == 1) {  // the next pair's h, both halves in one 32 B load
 #pragma unroll
-      for (int q = 0; q < NH; ++q) hbuf[b2][q] = __ldcg((q == 0 ? hp0 : hp1) + (sp + 2));
+        for (int q = 0; q < NH; ++q) ldcg_v8((q == 0 ? hp0 : hp1) + sp0 + 2, hbuf[0][q], hbuf[1][q]);
+      }
     }
     float z[G][8];
 #pragma unroll
@@ -1335,8 +1348,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
     uint32_t abytes = kAStage;
     const int kps = step_kps(st, kc_total, &abytes);
-    const uint32_t boff = kps > 1 ? kps * abytes : static_cast<uint32_t>(kAStage);  // B region of a stage
-    const uint32_t bchunk = static_cast<uint32_t>(ncols) * 128u;
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
       const bool bias_smem = bsrc != nullptr && st.cell != ED_CELL_LINEAR_OUT && st.gates * h * 4 <= kBiasBytes;
