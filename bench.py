@@ -534,7 +534,8 @@ def main():
             "config": {"workload": CONFIGS[args.config], **fsm_info, "instances_per_gpu": len(wl.graphs),
                        "nodes_per_gpu": wl.num_nodes, "batches": plan.info["num_batches"],
                        "lower_bound": plan.info["lower_bound"], "layout": args.layout, "step_order": args.step_order,
-                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world} ({args.scaling}; LPT by node count when strong)"},
+                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"instance-sharded x{world} ({args.scaling}; LPT by node count when strong)",
+                       "split_k_steps": plan.info["split_steps"], "grid": plan.query_info()["grid"]},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
                          "frac": achieved / P, "traffic": traffic,
                          "kernel": "ed_persistent_bf16" if wl.dtype == "bf16" else "ed_persistent_f32",

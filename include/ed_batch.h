@@ -191,6 +191,10 @@ typedef struct {
   int64_t h_rows;             /* rows of the H buffer: num_rows + staged operand rows           */
   double validate_us;         /* host time of validation + merge (part of plan_us)              */
   double lower_us;            /* host time of lowering (step table, index arrays, workspace map) */
+  int64_t split_steps;        /* bf16: device steps run split-K over a CTA pair:   */
+                              /*   each CTA of a 2-CTA cluster multiplies one K half; the pair     */
+                              /*   exchanges partial sums over distributed shared memory           */
+  int64_t grid;               /* CTAs of the persistent launch (0 until the first ed_execute)    */
 } ed_plan_info_t;
 
 /* Per weight set, device pointers.  Matrices must have been packed by ed_pack_weights.

@@ -155,6 +155,7 @@ struct ed_plan_s {
          off_h = 0, off_c = 0, off_y = 0, off_x = 0, off_u = 0, off_m = 0, ws_bytes = 0;
   int64_t y_cols = 0;
   bool need_x = false;
+  bool has_split = false;   // some step is split-K over a CTA pair (kernel launched with clusters of 2)
   bool need_mv = false;  // MV-RNN: U and Mx buffers
   // stats
   int64_t contig = 0, gather = 0, copy_bytes = 0, copy_kernels = 0;
@@ -491,6 +492,12 @@ static ed_status_t schedule(ed_plan_t *pl, const ed_fsm_t *fsm, int policy) {
 // ------------------------------------------------------------------------------------------------
 // lowering: node rows -> device step table
 // ------------------------------------------------------------------------------------------------
+// Split-K over CTA pairs; ED_SPLIT=0 turns it off (A/B development switch).
+static bool split_enabled() {
+  const char *v = std::getenv("ED_SPLIT");  // read per plan (tests switch it)
+  return !(v && std::atoi(v) == 0);
+}
+
 static ed_status_t lower(ed_plan_t *pl) {
   const int64_t V = pl->V;
   const int zero_row = static_cast<int32_t>(V);
@@ -506,6 +513,7 @@ static ed_status_t lower(ed_plan_t *pl) {
     return x;  // external id
   };
   pl->steps.clear();
+  pl->has_split = false;
   pl->op_rows = pl->staged = pl->staged_bytes = 0;
   std::vector<std::pair<int32_t, int32_t>> stage_pairs;  // (producer row, staged H row)
   const bool staging = pl->staging && pl->dtype == ED_BF16;
@@ -581,6 +589,15 @@ static ed_status_t lower(ed_plan_t *pl) {
       }
     }
     st.n_col_tiles = st.units > 0 ? (h + st.units - 1) / st.units : 0;
+    if (pl->dtype == ED_BF16 && st.units == 16 && h % 16 == 0 && ed::cell_splittable(ot.cell_kind) &&
+        (ed::cell_segments(ot.cell_kind) * h / 64) % 2 == 0 &&
+        2 * ((m + 127) / 128) * st.n_col_tiles <= 148 && split_enabled()) {
+      // split-K over a CTA pair (cluster of 2) for batches of at most half a wave of 16-unit tiles:
+      // each CTA streams half of the tile's K (half its operand and weight bytes, half the MMA
+      // chain) and runs the gate epilogue of one 8-unit half after a DSMEM exchange of partials
+      st.wsel |= ed::kStepSplitK;
+      pl->has_split = true;
+    }
     if (ot.cell_kind == ED_CELL_LINEAR_OUT && pl->dtype == ED_BF16) {
       // bf16 output linear on the tensor cores: one N = 16 column tile (C <= 16 classes, rows >= C
       // of the packed W_O are zero); units = C, gates = 1
@@ -1076,6 +1093,9 @@ ed_status_t ed_plan_info(const ed_plan_t *pl, ed_plan_info_t *o) {
   o->staged_operands = pl->staged;
   o->staged_bytes = pl->staged_bytes;
   o->h_rows = pl->V + 1 + pl->op_rows;
+  o->split_steps = 0;
+  for (const auto &st : pl->steps) o->split_steps += (st.wsel & ed::kStepSplitK) ? 1 : 0;
+  o->grid = pl->grid;
   return ED_OK;
 }
 
@@ -1223,7 +1243,7 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
     b.seq = seq = 1;
   }
   if (pl->grid == 0) {
-    e = ed::persistent_grid(pl->dtype, &pl->grid);
+    e = ed::persistent_grid(pl->dtype, pl->has_split, &pl->grid);
     if (e) return fail(ED_E_CUDA, std::string("occupancy: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
   }
   ed::KParams p;
@@ -1274,7 +1294,8 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
       }
     }
   }
-  e = ed::launch_persistent(p, pl->dtype, pl->grid, stream);
+  p.has_split = pl->has_split ? 1 : 0;
+  e = ed::launch_persistent(p, pl->dtype, pl->grid, pl->has_split, stream);
   if (e) return fail(ED_E_CUDA, std::string("launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
   return ED_OK;
 }

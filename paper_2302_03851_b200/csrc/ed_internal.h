@@ -20,7 +20,8 @@ constexpr int kCellTaggerOut = 102;    // y = W2 t + b2 of the BiLSTM tagger (t 
 // Node matrices are stored transposed (Mx row block of a node = M^T, row-major h x h).
 constexpr int kCellMvP = 103;
 constexpr int kCellMvMat = 104;
-constexpr int kMaxSlotsDev = 2;   // fixed slots the device reads (all cells have <= 2)
+constexpr int kMaxSlotsDev = 2;
+constexpr int kStepSplitK = 2;    // DevStep::wsel flag   // fixed slots the device reads (all cells have <= 2)
 
 // One batch of the schedule as the persistent kernel sees it (SoA-friendly 64 B record).
 // Slot j of member i (position i = ascending result row):
@@ -44,7 +45,9 @@ struct DevStep {
   int32_t n_col_tiles;// UMMA path: hidden / units
   int32_t gates;      // G: gate blocks of the main contraction
   int32_t nslots;     // fixed slots present
-  int32_t wsel;       // 0: weight set W/b, 1: second matrix W2/b2
+  int32_t wsel;       // bit 0 -- 0: weight set W/b, 1: second matrix W2/b2; bit 1 (kStepSplitK):
+                      // split-K over the CTA pair of a cluster (rank r multiplies K half r; the
+                      // pair exchanges the partial sums of each other's 8-unit half over DSMEM)
   int32_t self_need;  // readiness a row of this step's own output block must reach before the step
                       // may read it (= what earlier device steps of the same batch publish)
 };
@@ -97,6 +100,7 @@ struct alignas(64) KParams {
   uint32_t seq;               // launches of this plan on this workspace binding, 1, 2, ...
   int32_t ext_root_off;       // idx offset of (instance, external id) pairs of instances whose
   int32_t num_ext_roots;      // output is an input lookup (no op produces it)
+  int32_t has_split;          // some step is split-K over a CTA pair: launched with clusters of 2
   DevWeightSet w[kMaxWeightSets];
 };
 
@@ -165,6 +169,16 @@ inline bool cell_implemented(int cell) {
   }
 }
 
+// Cells whose 16-unit tiles may run split-K over a CTA pair (the device instantiates the split
+// epilogue for these only).
+inline bool cell_splittable(int cell) {
+  switch (cell) {
+    case ED_CELL_TREELSTM_INTERNAL:
+    case ED_CELL_TREEGRU_INTERNAL: return true;
+    default: return false;
+  }
+}
+
 // K segments (each of width hidden) of the main contraction.
 inline int cell_segments(int cell) {
   switch (cell) {
@@ -184,11 +198,11 @@ inline int step_contrib(int cell, int h) {
 }
 
 // Launch entry points implemented in ed_kernels.cu (return cudaError_t as int).
-int launch_persistent(const KParams &p, int dtype, int grid, void *stream);
+int launch_persistent(const KParams &p, int dtype, int grid, bool cluster2, void *stream);
 int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const float *src, void *dst,
                 void *stream);
 int64_t packed_bytes(int cell, int hidden, int out_dim, int dtype, int which);
 int device_check(int *sm_count, int *major, int *minor);
-int persistent_grid(int dtype, int *grid);
+int persistent_grid(int dtype, bool cluster2, int *grid);
 
 }  // namespace ed

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdio>
+#include <cstring>
 
 #include "ed_internal.h"
 
@@ -236,6 +237,49 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---- CTA-pair (cluster of 2) exchange for split-K steps ----
+// shared::cluster address of the same shared-memory object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// arrive on an mbarrier of another CTA of the cluster, ordering this thread's earlier accesses
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar), ok = 0, spins = 0;
+  do {
+    if (++spins > (1u << 30)) __trap();
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// 16 B into another CTA's shared memory; the bytes complete_tx on that CTA's mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, float a, float b, float c, float d,
+                                            uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cluster_addr),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(cluster_bar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_v4_b32(void *a, uint4 v) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart (SBO), version 1.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
@@ -265,6 +309,9 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
   return v;
 }
+#ifndef ED_WATCHDOG_PRINTF
+#define ED_WATCHDOG_PRINTF 0
+#endif
 #ifndef ED_POLL_NS
 #define ED_POLL_NS 32  // back-off between readiness polls
 #endif
@@ -288,9 +335,11 @@ __device__ __forceinline__ void wait_row(const KParams &p, int e, const DevStep 
   if (need <= 0) return;
   unsigned spins = 0;
   while (ready_since_launch(p, e, tgt) < need) {
-    if (++spins > (1u << 26)) {  // watchdog: report the stuck dependency, then abort the launch
+    if (++spins > (1u << 26)) {  // watchdog: a lost publication must not hang the GPU
+#if ED_WATCHDOG_PRINTF  // diagnostic build: report the stuck dependency (the printf costs registers)
       printf("ed_batch watchdog: block %d thread %d cell %d out_row0 %d row %d ready %d need %d\n", blockIdx.x,
              threadIdx.x, st.cell, st.out_row0, e, ready_since_launch(p, e, tgt), need);
+#endif
       __trap();
     }
 #if ED_POLL_NS > 0
@@ -397,11 +446,12 @@ template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 __device__ __forceinline__ const void *step_W(const KParams &p, const DevStep &st) {
-  return st.wsel ? p.w[st.wset].W2 : p.w[st.wset].W;
+  return (st.wsel & 1) ? p.w[st.wset].W2 : p.w[st.wset].W;
 }
 __device__ __forceinline__ const float *step_b(const KParams &p, const DevStep &st) {
-  return st.wsel ? p.w[st.wset].b2 : p.w[st.wset].b;
+  return (st.wsel & 1) ? p.w[st.wset].b2 : p.w[st.wset].b;
 }
+__device__ __forceinline__ bool step_split(const DevStep &st) { return (st.wsel & kStepSplitK) != 0; }
 
 // Pointer to the h-vector an operand entry refers to (row of H, or an external embedding row).
 template <typename T>
@@ -939,10 +989,25 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4 &v, float *out) {
 // accumulator, then per 8 units: tcgen05.ld -> gates (fp32, MUFU tanh.approx) -> vector stores.
 // Child / previous-state rows of the next 8-unit step are prefetched while the current one is
 // processed; bias comes from shared memory.
-template <int CELL>
+// Split-K pair exchange of one tile (rank < 0: the step is not split).  Rank r of the CTA pair
+// holds the partial sums of K half r for all 16 units of the tile and finalises the 8-unit half r:
+// it sends the other half's partials (G x 8 fp32 per row) into the partner's receive buffer with
+// st.async (complete_tx on the partner's xfull) once the partner has signalled xfree.
+struct XCtx {
+  int rank;             // cluster rank (0 / 1), or -1
+  uint32_t par;         // phase parity of xfull / xfree for this tile
+  uint64_t *xfree;      // local: the partner may write its buffer (partner arrives remotely)
+  uint64_t *xfull;      // local: the partner's partials have landed in recv
+  uint32_t rrecv;       // cluster address of the partner's receive buffer
+  uint32_t rxfull;      // cluster address of the partner's xfull
+  const float *recv;    // local receive buffer: float4 (q, row) at (q * 128 + row) * 4
+};
+
+template <int CELL, bool SPLIT = false>
 __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &st, uint32_t tacc, uint64_t *tfull_bar,
                                               uint32_t parity, int row_tile, int col_tile, int r,
-                                              const float *sbias, bool bias_smem, unsigned long long *tr = nullptr) {
+                                              const float *sbias, bool bias_smem, const XCtx &x,
+                                              unsigned long long *tr = nullptr) {
   using CC = CellCfg<CELL>;
   constexpr int G = CC::G, NC = CC::NC, NH = CC::NH;
   const int h = p.hidden;
@@ -1002,11 +1067,27 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   // A warp whose 32 rows all lie past m skips the pass loop: tcgen05.ld bandwidth (~64 B/clk per
   // SM) is shared by the four epilogue warps, so small-m tail tiles read TMEM for their live rows only.
   const bool warp_live = row_tile * kTileM + (r & ~31) < st.m;
+  if (SPLIT && warp_live) {
+    // split-K: send the partner's 8-unit half of this row's partial sums, then wait for ours
+    float zs[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) tmem_ld8(tacc + static_cast<uint32_t>(g * 16 + (x.rank ^ 1) * 8), zs[g]);
+    tmem_wait_ld();
+    mbar_wait_cluster(x.xfree, x.par);
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        st_async_v4(x.rrecv + static_cast<uint32_t>(((2 * g + q) * kTileM + r) * 16), zs[g][4 * q], zs[g][4 * q + 1],
+                    zs[g][4 * q + 2], zs[g][4 * q + 3], x.rxfull);
+    mbar_wait_cluster(x.xfull, x.par);
+  }
 #pragma unroll 1
   for (int sp0 = 0; sp0 < (warp_live ? nsteps : 0); sp0 += 2) {
   uint4 hlo = make_uint4(0, 0, 0, 0);  // bf16 h of the pair's first half, stored with the second
 #pragma unroll
   for (int b2 = 0; b2 < 2; ++b2) {
+    if (SPLIT && b2 != x.rank) continue;  // split-K: the partner finalises this half
     const int sp = sp0 + b2;
     const int gq = sp >> 1, half = sp & 1;
     float4 cc[NC > 0 ? 2 * NC : 1];
@@ -1027,6 +1108,15 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
 #pragma unroll
     for (int g = 0; g < G; ++g) tmem_ld8(tacc + static_cast<uint32_t>(gq * G * 16 + g * 16 + half * 8), z[g]);
     tmem_wait_ld();
+    if (SPLIT) {  // + the partner's partial sums of K half (rank ^ 1)
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float4 v = lds_f4(x.recv + ((2 * g + q) * kTileM + r) * 4);
+          z[g][4 * q] += v.x; z[g][4 * q + 1] += v.y; z[g][4 * q + 2] += v.z; z[g][4 * q + 3] += v.w;
+        }
+    }
     if (tr != nullptr && r == 0 && sp < 2) tr[4 + 2 * sp] = globaltimer();
     if (!valid) continue;
     const int j0 = jb + sp * 8;
@@ -1144,7 +1234,15 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
       const uint4 hv4 = make_uint4(packed[0], packed[1], packed[2], packed[3]);
       // the pair's two 8-unit halves are one 32 B run of the row: one 256-bit store per row and copy
       // (full L2 sectors instead of two half-sector writes)
-      if (b2 == 0) {
+      if (SPLIT) {  // split-K: one 8-unit half per CTA, 16 B per row and copy
+        st_v4_b32(H + orow * h + j0, hv4);
+        if (cpy0 != nullptr) st_v4_b32(cpy0 + j0, hv4);
+        if (cpy1 != nullptr) st_v4_b32(cpy1 + j0, hv4);
+        for (int d = dbeg; d < dend; ++d) {
+          __nv_bfloat16 *dst = copy_row<__nv_bfloat16>(p, __ldg(p.idx + d));
+          if (dst != nullptr) st_v4_b32(dst + j0, hv4);
+        }
+      } else if (b2 == 0) {
         hlo = hv4;
       } else {
         const int jp = j0 - 8;
@@ -1168,7 +1266,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   if (valid) {
     asm volatile("fence.proxy.async.global;" ::: "memory");  // rows may be read by TMA (async proxy)
     if (tr != nullptr && r == 0) tr[2] = globaltimer();
-    publish_row(p, static_cast<int>(orow), ngroups * 16);
+    publish_row(p, static_cast<int>(orow), SPLIT ? 8 : ngroups * 16);
     if (tr != nullptr && r == 0) tr[3] = globaltimer();
   }
 }
@@ -1241,7 +1339,7 @@ constexpr int kSimtRows = 2 * (kThreadsTC / 32);  // every warp of the CTA, 2 ro
 __device__ __forceinline__ int step_items(const DevStep &st, int h) {
   if (st.cell == kCellMvMat) return static_cast<int>((static_cast<long>(st.m) * h + kTileM - 1) / kTileM) * st.n_col_tiles;
   if (st.cell == ED_CELL_MVRNN_INTERNAL) return 2 * st.m;  // matvec: one CTA per (member, half)
-  if (is_umma_cell(st.cell)) return ((st.m + kTileM - 1) / kTileM) * st.n_col_tiles;
+  if (is_umma_cell(st.cell)) return ((st.m + kTileM - 1) / kTileM) * st.n_col_tiles * (step_split(st) ? 2 : 1);
   return (st.m + kSimtRows - 1) / kSimtRows;
 }
 // K chunks per pipeline stage.  One full/empty mbarrier round costs ~0.3 us whatever its payload
@@ -1275,6 +1373,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
                                                 kWoutBytes);
   uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = bars + 2 * kStages + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);
+  uint64_t *xfree = bars + 2 * kStages + 5, *xfull = bars + 2 * kStages + 6;  // split-K pair exchange
+  // split-K receive buffer (<= 128 rows x 5 gates x 8 units fp32 = 20 KB): aliases the bias and
+  // output-weight buffers, which split steps do not use (their bias is read from L2)
+  const float *xrecv = sbias;
+  static_assert(kBiasBytes + kWoutBytes >= kTileM * 5 * 8 * 4, "split-K receive buffer");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -1286,6 +1389,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, kEpiThreads);
     }
+    mbar_init(xfree, 1);
+    mbar_init(xfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 4) {
@@ -1294,6 +1399,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   }
   tc_fence_before();
   __syncthreads();
+  if (p.has_split) cluster_sync_all();  // the partner's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   prologue_checks<__nv_bfloat16>(p);
@@ -1311,8 +1417,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   // there is no grid barrier between steps (dataflow).
   if (warp < 4) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
+    uint32_t xcnt = 0;  // split tiles exchanged (xfull / xfree phase)
   for (int s = 0; s < p.num_steps; ++s) {
     const DevStep st = p.steps[s];
+    const bool split = step_split(st);
+    if (split) {  // pair items (2j, 2j + 1) on the two CTAs of a cluster: even rotation offset
+      off = (off + 1u) & ~1u;
+      if (off >= static_cast<uint32_t>(G)) off -= static_cast<uint32_t>(G);
+    }
     const int T = step_items(st, h);
     const int t0 = first_item(off);
     off = (off + static_cast<uint32_t>(T)) % static_cast<uint32_t>(G);
@@ -1328,6 +1440,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
       const int C = st.gates;
       const bool in_smem = C * h * 4 <= kWoutBytes;
+      if (p.has_split) __syncthreads();  // swout may still hold a split-K exchange of the epilogue
       if (in_smem) {  // 16 B cp.async per piece (no register staging)
         const float *W = static_cast<const float *>(step_W(p, st));
         const uint32_t sw = smem_u32(swout);
@@ -1347,10 +1460,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const int ncols = st.cell == ED_CELL_LINEAR_OUT ? 16 : st.gates * st.units;
     const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
     uint32_t abytes = kAStage;
-    const int kps = step_kps(st, kc_total, &abytes);
+    const int kc_part = split ? kc_total / 2 : kc_total;  // K chunks per CTA
+    const int kps = step_kps(st, kc_part, &abytes);
       // ---------------- epilogue warps ----------------
       const float *bsrc = step_b(p, st);
-      const bool bias_smem = bsrc != nullptr && st.cell != ED_CELL_LINEAR_OUT && st.gates * h * 4 <= kBiasBytes;
+      const bool bias_smem = !split && bsrc != nullptr && st.cell != ED_CELL_LINEAR_OUT && st.gates * h * 4 <= kBiasBytes;
       if (bias_smem) {  // 16 B cp.async per piece: no register staging, all pieces in flight at once
         const uint32_t sb = smem_u32(sbias);
         for (int q = tid; q < st.gates * h / 4; q += kEpiThreads) cp_async16(sb + 16u * q, bsrc + 4 * q);
@@ -1362,39 +1476,73 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       for (int t = t0; t < T; t += G) {
         const uint32_t acc = pipe.ti & 1u;
         const uint32_t tacc = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * 256u;
-        const int row_tile = t / st.n_col_tiles, col_tile = t % st.n_col_tiles;
+        const int tile = split ? (t >> 1) : t;
+        const int row_tile = tile / st.n_col_tiles, col_tile = tile % st.n_col_tiles;
         const uint32_t par = (pipe.ti >> 1) & 1u;
+        XCtx x;
+        x.rank = -1;
+#ifndef ED_NO_SPLIT
+        if (split) {
+          // the receive buffer is free once every epilogue thread is past the previous exchange
+          asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
+          const uint32_t crank = static_cast<uint32_t>(t & 1);  // = %cluster_ctarank (even rotation offset)
+          x.rank = static_cast<int>(crank);
+          x.par = xcnt & 1u;
+          ++xcnt;
+          x.xfree = xfree;
+          x.xfull = xfull;
+          x.rrecv = mapa_u32(smem_u32(xrecv), crank ^ 1u);
+          x.rxfull = mapa_u32(smem_u32(xfull), crank ^ 1u);
+          x.recv = xrecv;
+          if (tid == 0) {
+            const int live = min(4, (st.m - row_tile * kTileM + 31) / 32);  // warps with rows
+            mbar_arrive_tx(xfull, static_cast<uint32_t>(live * 32 * st.gates * 8 * 4));
+            mbar_arrive_remote(mapa_u32(smem_u32(xfree), crank ^ 1u));  // the partner may now write our buffer
+          }
+        }
+#endif
+#ifndef ED_NO_SPLIT
+        if (split) {  // split-K steps (cells of ed::cell_splittable)
+          unsigned long long *trp = (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr;
+          switch (st.cell) {
+            case ED_CELL_TREELSTM_INTERNAL:
+              umma_epilogue<ED_CELL_TREELSTM_INTERNAL, true>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, false, x, trp); break;
+            default:
+              umma_epilogue<ED_CELL_TREEGRU_INTERNAL, true>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, false, x, trp); break;
+          }
+        } else
+#endif
         switch (st.cell) {
           case ED_CELL_TREELSTM_LEAF:
-            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREELSTM_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREELSTM_INTERNAL:
-            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREELSTM_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEGRU_LEAF:
-            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREEGRU_LEAF>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEGRU_INTERNAL:
-            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREEGRU_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_TREEFC_INTERNAL:
-            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TREEFC_INTERNAL>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LSTM:
-            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LSTM>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_CHAR:
-            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICE_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICEGRU_CHAR:
-            umma_epilogue<ED_CELL_LATTICEGRU_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICEGRU_CHAR>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICEGRU_WORD:
-            umma_epilogue<ED_CELL_LATTICEGRU_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICEGRU_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case ED_CELL_LATTICE_WORD:
-            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_LATTICE_WORD>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellLatticeLink:
-            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<kCellLatticeLink>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvP:
-            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<kCellMvP>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
           case kCellMvMat:
             mv_mat_epilogue(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid); break;
           case ED_CELL_LINEAR_OUT:
             linear_out_epilogue(p, st, tacc, tfull + acc, par, row_tile, tid); break;
           default:
-            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
+            umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
         }
         ED_TRACE(p, s, 5, tid == 0 && t == 0);
         tc_fence_before();
@@ -1408,6 +1556,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
   for (int s = 0; s < p.num_steps; ++s) {
     const DevStep st = p.steps[s];
+    const bool split = step_split(st);
+    if (split) {  // pair items (2j, 2j + 1) on the two CTAs of a cluster: even rotation offset
+      off = (off + 1u) & ~1u;
+      if (off >= static_cast<uint32_t>(G)) off -= static_cast<uint32_t>(G);
+    }
     const int T = step_items(st, h);
     const int t0 = first_item(off);
     off = (off + static_cast<uint32_t>(T)) % static_cast<uint32_t>(G);
@@ -1423,6 +1576,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
       // ---------------- SIMT step (output linear / tagger output): every warp, 2 rows each ----------
       const int C = st.gates;
       const bool in_smem = C * h * 4 <= kWoutBytes;
+      if (p.has_split) __syncthreads();  // swout may still hold a split-K exchange of the epilogue
       if (in_smem) {  // 16 B cp.async per piece (no register staging)
         const float *W = static_cast<const float *>(step_W(p, st));
         const uint32_t sw = smem_u32(swout);
@@ -1442,21 +1596,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
     const int ncols = st.cell == ED_CELL_LINEAR_OUT ? 16 : st.gates * st.units;
     const int kc_total = (cell_segments_dev(st.cell) * h) / kChunkK;
     uint32_t abytes = kAStage;
-    const int kps = step_kps(st, kc_total, &abytes);
+    const int kc_part = split ? kc_total / 2 : kc_total;  // K chunks per CTA
+    const int kps = step_kps(st, kc_part, &abytes);
     const uint32_t boff = kps > 1 ? kps * abytes : static_cast<uint32_t>(kAStage);  // B region of a stage
     const uint32_t bchunk = static_cast<uint32_t>(ncols) * 128u;
 if (warp == 4) {
       // ---------------- MMA issuer ----------------
       for (int t = t0; t < T; t += G) {
         const uint32_t acc = pipe.ti & 1u;
-        const uint32_t idesc = idesc_bf16(tile_cols(st, h, t % st.n_col_tiles));
+        const int tile = split ? (t >> 1) : t;
+        const int kbeg = split ? (t & 1) * kc_part : 0, kend = kbeg + kc_part;
+        const uint32_t idesc = idesc_bf16(tile_cols(st, h, tile % st.n_col_tiles));
         // the whole warp walks the loop (warp-uniform operands); one elected lane issues
         mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * 256u;
         const uint64_t astep = abytes >> 4, bstep = bchunk >> 4;  // descriptor address units (16 B)
-        for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
-          const int nk = min(kps, kc_total - kc0);
+        for (int kc0 = kbeg; kc0 < kend; kc0 += kps) {
+          const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
           mbar_wait(full + stg, (pipe.it / kStages) & 1u);
           fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
@@ -1467,7 +1624,7 @@ if (warp == 4) {
           for (int q = 0; q < nk; ++q, ad += astep, bd += bstep) {
 #pragma unroll
             for (int k = 0; k < kChunkK / 16; ++k)
-              tc_mma_elect(d, ad + 2 * k, bd + 2 * k, idesc, (kc0 + q > 0 || k > 0) ? 1u : 0u);
+              tc_mma_elect(d, ad + 2 * k, bd + 2 * k, idesc, (kc0 + q > kbeg || k > 0) ? 1u : 0u);
           }
           tc_commit_elect(empty + stg);
           ++pipe.it;
@@ -1481,10 +1638,11 @@ if (warp == 4) {
       const uint8_t *Wp = static_cast<const uint8_t *>(step_W(p, st));
       const size_t ntot = st.cell == ED_CELL_LINEAR_OUT ? 16 : static_cast<size_t>(st.gates) * h;
       for (int t = t0; t < T; t += G) {  // warp-converged; one elected lane issues
-        const int col_tile = t % st.n_col_tiles;
+        const int col_tile = (split ? (t >> 1) : t) % st.n_col_tiles;
+        const int kbeg = split ? (t & 1) * kc_part : 0, kend = kbeg + kc_part;
         const uint32_t nb = static_cast<uint32_t>(tile_cols(st, h, col_tile)) * 128u;
-        for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
-          const int nk = min(kps, kc_total - kc0);
+        for (int kc0 = kbeg; kc0 < kend; kc0 += kps) {
+          const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
           mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
           mbar_arrive_tx_elect(full + stg, nb * nk);
@@ -1552,7 +1710,8 @@ if (warp == 4) {
         continue;
       }
       for (int t = t0; t < T; t += G) {
-        const int row_tile = t / st.n_col_tiles;
+        const int row_tile = (split ? (t >> 1) : t) / st.n_col_tiles;
+        const int kbeg = split ? (t & 1) * kc_part : 0, kend = kbeg + kc_part;
         const void **tab = rowtab + (tab_tile & 1u) * (kTileM * 2);
         ++tab_tile;
         int ent[2][2];  // this thread's input rows (at most 2 rows x 2 segments)
@@ -1583,8 +1742,9 @@ if (warp == 4) {
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // published rows may be read by TMA
         };
-        acquire_seg(0);
-        int acquired = 1;  // segments [0, acquired) are acquired
+        const int sg0 = kbeg * kChunkK >= h ? 1 : 0;  // first K segment of this CTA's range
+        acquire_seg(sg0);
+        int acquired = sg0 + 1;  // segments [sg0, acquired) are acquired
         if (lt == 0) ED_TRACE(p, s, 1, t == 0);
         const int nrows = min(kTileM, st.m - row_tile * kTileM);
         const int pieces = nrows * 8;  // 16 B pieces per K chunk
@@ -1593,8 +1753,8 @@ if (warp == 4) {
 #pragma unroll
         for (int sg = 0; sg < 2; ++sg)
           if (sg < nseg && !segment_contig(p, st, sg, &cb[sg])) cb[sg] = -1;
-        for (int kc0 = 0; kc0 < kc_total; kc0 += kps) {
-          const int nk = min(kps, kc_total - kc0);
+        for (int kc0 = kbeg; kc0 < kend; kc0 += kps) {
+          const int nk = min(kps, kend - kc0);
           if (acquired < 2 && (kc0 + nk - 1) * kChunkK >= h) {  // the stage reaches segment 1
             acquire_seg(1);
             acquired = 2;
@@ -1650,6 +1810,7 @@ if (warp == 4) {
   tc_fence_before();
   __syncthreads();
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  if (p.has_split) cluster_sync_all();  // no CTA leaves while its partner may still address it
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1790,7 +1951,25 @@ int device_check(int *sm_count, int *major, int *minor) {
   return static_cast<int>(e);
 }
 
-int persistent_grid(int dtype, int *grid) {
+// Launch configuration of a plan with split-K steps: clusters of 2 CTAs (one per SM).
+static void cluster2_config(cudaLaunchConfig_t *cfg, cudaLaunchAttribute *at, int grid, cudaStream_t s,
+                            bool cooperative) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->gridDim = dim3(grid);
+  cfg->blockDim = dim3(kThreadsTC);
+  cfg->dynamicSmemBytes = kSmemBytes;
+  cfg->stream = s;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg->attrs = at;
+  cfg->numAttrs = cooperative ? 2 : 1;
+}
+
+int persistent_grid(int dtype, bool cluster2, int *grid) {
   int sms = 0, major = 0, minor = 0;
   int e = device_check(&sms, &major, &minor);
   if (e) return e;
@@ -1801,6 +1980,17 @@ int persistent_grid(int dtype, int *grid) {
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ed_persistent_bf16, kThreadsTC, kSmemBytes);
     if (ce != cudaSuccess) return static_cast<int>(ce);
     if (per_sm > 1) per_sm = 1;  // TMEM: one 512-column allocation per SM
+    if (cluster2) {
+      // every CTA must be resident at once (dataflow waits): as many pairs as fit together
+      cudaLaunchConfig_t cfg;
+      cudaLaunchAttribute at[2];
+      cluster2_config(&cfg, at, 2 * (sms / 2), nullptr, false);
+      int clusters = 0;
+      ce = cudaOccupancyMaxActiveClusters(&clusters, ed_persistent_bf16, &cfg);
+      if (ce != cudaSuccess) return static_cast<int>(ce);
+      *grid = 2 * (clusters < sms / 2 ? clusters : sms / 2);
+      return *grid > 0 ? 0 : static_cast<int>(cudaErrorLaunchOutOfResources);
+    }
   } else {
     cudaError_t ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ed_persistent_f32, kThreads, 0);
     if (ce != cudaSuccess) return static_cast<int>(ce);
@@ -1810,11 +2000,21 @@ int persistent_grid(int dtype, int *grid) {
   return 0;
 }
 
-int launch_persistent(const KParams &p, int dtype, int grid, void *stream) {
+int launch_persistent(const KParams &p, int dtype, int grid, bool cluster2, void *stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   void *args[] = {const_cast<KParams *>(&p)};
-  if (dtype == ED_BF16) {
+  if (dtype == ED_BF16 && cluster2) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute at[2];
+    cluster2_config(&cfg, at, grid, s, true);
+    e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(ed_persistent_bf16), args);
+    if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported) {  // cooperative + cluster not accepted:
+      (void)cudaGetLastError();                                       // the grid is sized to be co-resident
+      cluster2_config(&cfg, at, grid, s, false);
+      e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(ed_persistent_bf16), args);
+    }
+  } else if (dtype == ED_BF16) {
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void *>(ed_persistent_bf16), dim3(grid), dim3(kThreadsTC), args,
                                     kSmemBytes, s);
   } else {

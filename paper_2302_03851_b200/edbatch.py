@@ -70,7 +70,8 @@ class ed_plan_info_t(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in _INFO_I64] + [
         ("plan_us", ctypes.c_double), ("schedule_us", ctypes.c_double), ("layout_us", ctypes.c_double),
         ("staged_operands", ctypes.c_int64), ("staged_bytes", ctypes.c_int64), ("h_rows", ctypes.c_int64),
-        ("validate_us", ctypes.c_double), ("lower_us", ctypes.c_double)]
+        ("validate_us", ctypes.c_double), ("lower_us", ctypes.c_double), ("split_steps", ctypes.c_int64),
+        ("grid", ctypes.c_int64)]
 
 
 class ed_weight_set_t(ctypes.Structure):
@@ -276,6 +277,12 @@ class Plan:
         info = ed_plan_info_t()
         _check(LIB.ed_plan_info(handle, ctypes.byref(info)))
         self.info = {n: getattr(info, n) for n, _ in ed_plan_info_t._fields_}
+
+    def query_info(self) -> dict:
+        """ed_plan_info now (grid is set by the first ed_execute)."""
+        info = ed_plan_info_t()
+        _check(LIB.ed_plan_info(self.handle, ctypes.byref(info)))
+        return {n: getattr(info, n) for n, _ in ed_plan_info_t._fields_}
 
     def __del__(self):
         if getattr(self, "handle", None) and LIB is not None:
