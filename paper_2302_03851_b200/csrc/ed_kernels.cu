@@ -1545,6 +1545,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
             umma_epilogue<ED_CELL_TAGGER>(p, st, tacc, tfull + acc, par, row_tile, col_tile, tid, bias, bias_smem, x, (p.trace && t == 0) ? p.trace + s * 64 + 6 : nullptr); break;
         }
         ED_TRACE(p, s, 5, tid == 0 && t == 0);
+#ifdef ED_LEAF_TRACE  // development: per-CTA end of each of the first step's tiles
+        if (p.trace && s == 0 && tid == 0) {
+          const int k = (t - t0) / G;
+          if (k < 4) p.trace[p.num_steps * 64 + blockIdx.x * 4 + k] = globaltimer();
+        }
+#endif
         tc_fence_before();
         mbar_arrive(tempty + acc);
         ++pipe.ti;
