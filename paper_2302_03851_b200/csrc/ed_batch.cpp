@@ -65,15 +65,22 @@ double now_us() {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Pinned staging buffer for the async H2D upload of a plan's static part (step table, index
-// arrays).  Reused across plans: before it is overwritten the previous copy must have completed
-// (an event recorded after it), so a new minibatch plan needs no cudaMallocHost.
-struct Staging {
-  std::mutex mu;
+// Pinned staging buffers for the async H2D upload of a plan's static part (step table, index
+// arrays): a ring of kStagingSlots buffers, so the host can upload the next minibatches' plans
+// while earlier kernels still run on the stream (a slot is reused once the copy recorded on it has
+// completed; with one buffer every upload waited for the previous kernel).  A new minibatch plan
+// needs no cudaMallocHost.
+constexpr int kStagingSlots = 4;
+struct StagingSlot {
   void *buf = nullptr;
   size_t cap = 0;
   cudaEvent_t done = nullptr;
   bool pending = false;
+};
+struct Staging {
+  std::mutex mu;
+  StagingSlot slot[kStagingSlots];
+  int next = 0;
 };
 Staging &staging() {
   static Staging s;
@@ -81,8 +88,10 @@ Staging &staging() {
 }
 
 cudaError_t upload_async(void *dst, const void *src, size_t n, cudaStream_t s) {
-  Staging &st = staging();
-  std::lock_guard<std::mutex> lk(st.mu);
+  Staging &stg = staging();
+  std::lock_guard<std::mutex> lk(stg.mu);
+  StagingSlot &st = stg.slot[stg.next];
+  stg.next = (stg.next + 1) % kStagingSlots;
   cudaError_t e = cudaSuccess;
   if (st.pending) {
     e = cudaEventSynchronize(st.done);

@@ -23,6 +23,7 @@
 #include <stdint.h>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "ed_internal.h"
 
@@ -1651,11 +1652,16 @@ if (warp == 4) {
           const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
           mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
-          mbar_arrive_tx_elect(full + stg, nb * nk);
+#ifdef ED_EXP_HALFB  // experiment (wrong results): the first step loads half of each B chunk
+          const uint32_t nbx = s == 0 ? nb / 2 : nb;
+#else
+          const uint32_t nbx = nb;
+#endif
+          mbar_arrive_tx_elect(full + stg, nbx * nk);
           for (int q = 0; q < nk; ++q) {
             const uint8_t *src =
                 Wp + ((static_cast<size_t>(kc0 + q) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-            bulk_g2s_elect(stages + stg * kStageBytes + boff + q * bchunk, src, nb, full + stg);
+            bulk_g2s_elect(stages + stg * kStageBytes + boff + q * bchunk, src, nbx, full + stg);
           }
           ++pipe.it;
         }
@@ -2013,7 +2019,11 @@ int launch_persistent(const KParams &p, int dtype, int grid, bool cluster2, void
   if (dtype == ED_BF16 && cluster2) {
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[2];
-    cluster2_config(&cfg, at, grid, s, true);
+    // Not a cooperative launch: ncu cannot replay cooperative cluster launches (LaunchFailed), and
+    // the grid is sized by cudaOccupancyMaxActiveClusters so that every pair is resident at once on
+    // an idle GPU (the dataflow waits need that).  ED_CLUSTER_COOP=1 asks for the cooperative form.
+    static const bool coop = std::getenv("ED_CLUSTER_COOP") && std::atoi(std::getenv("ED_CLUSTER_COOP")) == 1;
+    cluster2_config(&cfg, at, grid, s, coop);
     e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(ed_persistent_bf16), args);
     if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported) {  // cooperative + cluster not accepted:
       (void)cudaGetLastError();                                       // the grid is sized to be co-resident
