@@ -129,19 +129,28 @@ inline int cell_gates(int cell) {
 // Hidden units per column tile on the bf16 tensor-core path (N tile = gates * units <= 256); the
 // last column tile of a row holds the remaining h % units units.  Fixed per cell kind so that host
 // tiling and the device epilogue templates agree.
+#ifndef ED_MAX_TILE_N
+#define ED_MAX_TILE_N 256  // widest MMA N tile (B stage = N x 128 B)
+#endif
+inline int cell_units_max(int cell);
 inline int cell_units(int cell) {
+  const int u = cell_units_max(cell), g = cell_gates(cell);
+  if (u <= 0 || g <= 0 || g * u <= ED_MAX_TILE_N) return u;
+  return (ED_MAX_TILE_N / g) / 16 * 16;
+}
+inline int cell_units_max(int cell) {
   switch (cell) {
     case ED_CELL_TREELSTM_LEAF: return 80;      // N = 240
     case ED_CELL_TREELSTM_INTERNAL: return 48;  // N = 240
     case ED_CELL_TREEGRU_LEAF: return 128;      // N = 256
     case ED_CELL_TREEGRU_INTERNAL: return 48;   // N = 240
-    case ED_CELL_TREEFC_INTERNAL: return 256;   // N = 256
+    case ED_CELL_TREEFC_INTERNAL: return 192;   // N = 192 (measured faster than 256)
     case ED_CELL_LSTM: return 64;               // N = 256
     case ED_CELL_LATTICE_CHAR: return 64;       // N = 256
     case ED_CELL_LATTICE_WORD: return 80;       // N = 240
     case ED_CELL_LATTICEGRU_CHAR:
     case ED_CELL_LATTICEGRU_WORD: return 64;    // N = 256
-    case kCellLatticeLink: return 256;          // N = 256
+    case kCellLatticeLink: return 192;          // N = 192 (measured faster than 256)
     case ED_CELL_TAGGER: return 256;            // N = 256
     case kCellMvP: return 256;                  // N = 256
     case kCellMvMat: return 256;                // N = 256 (columns of P^T)

@@ -38,16 +38,22 @@ constexpr int kThreads = 256;        // fp32 SIMT kernel
 #endif
 constexpr int kLoaderThreads = ED_LOADER_WARPS * 32;  // warps 6.. (operand gathers)
 constexpr int kThreadsTC = 192 + kLoaderThreads;      // bf16 tensor-core kernel: 4 epilogue, MMA, B, loaders
-constexpr int kStages = 4;
+#ifndef ED_STAGES
+#define ED_STAGES 4
+#endif
+constexpr int kStages = ED_STAGES;
 constexpr int kTileM = 128;
 constexpr int kChunkK = 64;                  // bf16 elements per 128 B swizzle row
 constexpr int kAStage = kTileM * 128;        // 16 KB
-constexpr int kBStage = 256 * 128;           // 32 KB (N tile <= 256)
+constexpr int kBStage = ED_MAX_TILE_N * 128;  // 32 KB (N tile <= 256)
 constexpr int kStageBytes = kAStage + kBStage;
 constexpr int kRowTab = kTileM * 2 * 8;      // row pointers per tile (2 segments)
 constexpr int kBiasBytes = 5 * 512 * 4;           // G * h fp32 (G * h <= 2560)
 constexpr int kWoutBytes = 12 * 1024;             // output-linear weights [C][h] fp32 (else read from L2)
-constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kRowTab + kBiasBytes + kWoutBytes + 256;
+#ifndef ED_SMEM_SLACK
+#define ED_SMEM_SLACK 1024  // alignment slack of the dynamic shared memory base
+#endif
+constexpr int kSmemBytes = ED_SMEM_SLACK + kStages * kStageBytes + 2 * kRowTab + kBiasBytes + kWoutBytes + 256;
 constexpr int kEpiThreads = 128;
 // setmaxnreg budgets (multiples of 8): 128 x kEpiRegs + 256 x kProdRegs <= 64K registers per SM
 #ifndef ED_EPI_REGS
@@ -73,14 +79,29 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef ED_TEST_WAIT
+#define ED_TEST_WAIT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar), ok = 0, spins = 0;
   do {
     if (++spins > (1u << 30)) __trap();  // watchdog: a lost arrival must not hang the GPU
+#if ED_TEST_WAIT  // non-blocking probe (no suspend / resume of the waiting thread)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    continue;
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
@@ -88,6 +109,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "r"(addr), "r"(parity)
         : "memory");
   } while (!ok);
+}
+// Warp-wide wait: one lane polls the barrier, the warp then reconverges (fewer try_wait probes
+// competing for the barrier / shared-memory pipe than 32 polling lanes).
+#ifndef ED_LANE0_POLL
+#define ED_LANE0_POLL 0
+#endif
+__device__ __forceinline__ void mbar_wait_warp(uint64_t *bar, uint32_t parity) {
+#if ED_LANE0_POLL
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -312,6 +346,9 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
 }
 #ifndef ED_WATCHDOG_PRINTF
 #define ED_WATCHDOG_PRINTF 0
+#endif
+#ifndef ED_TMA_ONE_ARRIVE
+#define ED_TMA_ONE_ARRIVE 0  // measured neutral
 #endif
 #ifndef ED_POLL_NS
 #define ED_POLL_NS 32  // back-off between readiness polls
@@ -1060,7 +1097,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   }
 #pragma unroll
   for (int q = 0; q < NH; ++q) ldcg_v8(q == 0 ? hp0 : hp1, hbuf[0][q], hbuf[1][q]);  // both halves of pair 0
-  mbar_wait(tfull_bar, parity);
+  mbar_wait_warp(tfull_bar, parity);
   tc_fence_after();
   if (tr != nullptr && r == 0) *tr = globaltimer();
   __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
@@ -1084,7 +1121,11 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
     mbar_wait_cluster(x.xfull, x.par);
   }
 #pragma unroll 1
+#ifdef ED_EXP_NOEPI  // experiment (wrong results): the leaf's epilogue does no pass
+  for (int sp0 = 0; sp0 < (warp_live && CELL != ED_CELL_TREELSTM_LEAF ? nsteps : 0); sp0 += 2) {
+#else
   for (int sp0 = 0; sp0 < (warp_live ? nsteps : 0); sp0 += 2) {
+#endif
   uint4 hlo = make_uint4(0, 0, 0, 0);  // bf16 h of the pair's first half, stored with the second
 #pragma unroll
   for (int b2 = 0; b2 < 2; ++b2) {
@@ -1366,6 +1407,9 @@ __device__ __forceinline__ int first_item(uint32_t off) {
 __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid_constant__ KParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+#if ED_SMEM_SLACK == 0
+  if (smem != smem_raw) __trap();  // built without alignment slack: the base must be 1024-aligned
+#endif
   uint8_t *stages = smem;
   const void **rowtab = reinterpret_cast<const void **>(smem + kStages * kStageBytes);  // [2][128][2] row ptrs
   float *sbias = reinterpret_cast<float *>(smem + kStages * kStageBytes + 2 * kRowTab);
@@ -1404,6 +1448,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) ed_persistent_bf16(const __grid
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   prologue_checks<__nv_bfloat16>(p);
+#if ED_PREFETCH_TMAP
+  if (tid == 192) {  // the operand loaders' descriptors into the TMA descriptor cache
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tm_h128)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tm_u)) : "memory");
+  }
+#endif
   if (blockIdx.x == 0 && tid == 0) p.ts[0] = globaltimer();
 
   const int h = p.hidden;
@@ -1615,17 +1665,20 @@ if (warp == 4) {
         const int kbeg = split ? (t & 1) * kc_part : 0, kend = kbeg + kc_part;
         const uint32_t idesc = idesc_bf16(tile_cols(st, h, tile % st.n_col_tiles));
         // the whole warp walks the loop (warp-uniform operands); one elected lane issues
-        mbar_wait(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
+        mbar_wait_warp(tempty + acc, ((pipe.ti >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * 256u;
         const uint64_t astep = abytes >> 4, bstep = bchunk >> 4;  // descriptor address units (16 B)
         for (int kc0 = kbeg; kc0 < kend; kc0 += kps) {
           const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
-          mbar_wait(full + stg, (pipe.it / kStages) & 1u);
+          mbar_wait_warp(full + stg, (pipe.it / kStages) & 1u);
           fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
           tc_fence_after();
           ED_TRACE(p, s, 3, lane == 0 && kc0 == 0 && t == 0);
+#ifdef ED_CHUNK_TRACE  // development: when each stage of item 0 became full (MMA side)
+          ED_TRACE(p, s, 32 + min(15, (kc0 - kbeg) / kps), lane == 0 && t == 0);
+#endif
           const uint32_t sbase = smem_u32(stages + stg * kStageBytes);
           uint64_t ad = sw128_desc(sbase), bd = sw128_desc(sbase + boff);
           for (int q = 0; q < nk; ++q, ad += astep, bd += bstep) {
@@ -1651,9 +1704,12 @@ if (warp == 4) {
         for (int kc0 = kbeg; kc0 < kend; kc0 += kps) {
           const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
-          mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+          mbar_wait_warp(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+#ifdef ED_CHUNK_TRACE  // development: when the weight loader got each stage of item 0
+          ED_TRACE(p, s, 11 + min(15, (kc0 - kbeg) / kps), lane == 0 && t == 0);
+#endif
 #ifdef ED_EXP_HALFB  // experiment (wrong results): the first step loads half of each B chunk
-          const uint32_t nbx = s == 0 ? nb / 2 : nb;
+          const uint32_t nbx = (s >= 1 && s <= 6) ? nb / 2 : nb;
 #else
           const uint32_t nbx = nb;
 #endif
@@ -1702,7 +1758,7 @@ if (warp == 4) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
           for (int kc = 0; kc < kc_total; ++kc) {
             const uint32_t stg = pipe.it % kStages;
-            mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+            mbar_wait_warp(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
             const int seg = (kc * kChunkK) / h, col0 = (kc * kChunkK) % h;
             uint8_t *a_dst = stages + stg * kStageBytes;
             if (lt == 0) {
@@ -1767,12 +1823,19 @@ if (warp == 4) {
           if (sg < nseg && !segment_contig(p, st, sg, &cb[sg])) cb[sg] = -1;
         for (int kc0 = kbeg; kc0 < kend; kc0 += kps) {
           const int nk = min(kps, kend - kc0);
+#ifdef ED_CHUNK_TRACE
+          ED_TRACE(p, s, 27, lt == 0 && t == 0 && kc0 == kbeg + 4);
+#endif
           if (acquired < 2 && (kc0 + nk - 1) * kChunkK >= h) {  // the stage reaches segment 1
             acquire_seg(1);
             acquired = 2;
           }
           const uint32_t stg = pipe.it % kStages;
-          mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+          bool tma_stage = false;
+          mbar_wait_warp(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+#ifdef ED_CHUNK_TRACE  // development: when the operand loaders got each stage of item 0
+          ED_TRACE(p, s, 48 + min(15, (kc0 - kbeg) / kps), lt == 0 && t == 0);
+#endif
           if (nk > 1) {  // several small chunks per stage: row gathers only (a 128-row box would overflow)
             if (lt == 0) mbar_arrive(full + stg);
             // the stage's nk x nrows x 8 pieces spread over all loader threads (a one-row tile puts
@@ -1792,6 +1855,7 @@ if (warp == 4) {
           uint8_t *a_dst = stages + stg * kStageBytes;
           // a 128-row box needs the full 16 KB A region: only with one chunk per stage (kps == 1)
           const int cbase = kps == 1 ? (seg == 0 ? cb[0] : cb[1]) : -1;
+          tma_stage = cbase >= 0;
           if (cbase >= 0) {
             if (lt < 32) {  // warp-converged; one elected lane issues
               mbar_arrive_tx_elect(full + stg, kAStage);
@@ -1799,19 +1863,43 @@ if (warp == 4) {
                 tma_row_box_elect(a_dst, &p.tm_u, seg * h + col0, cbase + row_tile * kTileM, full + stg);
               else
                 tma_row_box_elect(a_dst, &p.tm_h128, col0, cbase + row_tile * kTileM, full + stg);
+#ifdef ED_CHUNK_TRACE
+              ED_TRACE(p, s, 28, lt == 0 && t == 0 && kc0 == kbeg + 4);
+#endif
             }
           } else {
             if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
             const uint32_t a_base = smem_u32(a_dst);
-            for (int c = lt; c < nrows * 8; c += kLoaderThreads) {  // rows past m are not loaded
+#ifdef ED_EXP_HALFA  // experiment (wrong results): the first step gathers half of each A chunk
+            const int nrows_x = (s >= 1 && s <= 6) ? nrows / 2 : nrows;
+#else
+            const int nrows_x = nrows;
+#endif
+            for (int c = lt; c < nrows_x * 8; c += kLoaderThreads) {  // rows past m are not loaded
               const int r = c >> 3, ch = c & 7;
               const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(lds_ptr(tab + r * 2 + seg)) + col0 + ch * 8;
               cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
             }
           }
           }
-          // the stage completes when this thread's gathers have landed (no software lag)
+          // the stage completes when this thread's gathers have landed (no software lag); a stage
+          // read by TMA only takes one arrival standing for every loader thread (the per-thread
+          // mbarrier arrivals are serialised by the barrier: ~0.45 us per stage for 192 threads)
+#ifdef ED_CHUNK_TRACE
+          ED_TRACE(p, s, 29, lt == 0 && t == 0 && kc0 == kbeg + 4);
+#endif
+#if ED_TMA_ONE_ARRIVE
+          if (tma_stage) {
+            if (lt == 0) mbar_arrive_cnt(full + stg, kLoaderThreads);
+          } else {
+            cp_async_arrive_noinc(full + stg);
+          }
+#else
           cp_async_arrive_noinc(full + stg);
+#endif
+#ifdef ED_CHUNK_TRACE
+          ED_TRACE(p, s, 30, lt == 0 && t == 0 && kc0 == kbeg + 4);
+#endif
           ++pipe.it;
         }
         if (lt == 0) ED_TRACE(p, s, 2, t == 0);

@@ -31,4 +31,4 @@ for s in range(nb):
     print("  A stage free:", [rel(k) for k in range(48, 64) if t[s, k]])
     print("  B stage free:", [rel(k) for k in range(11, 27) if t[s, k]])
     print("  stage full:  ", [rel(k) for k in range(32, 48) if t[s, k]])
-    print("  stage1 A: arrive_tx/tma/pre-noinc/post-noinc:", [rel(k) for k in range(27, 32)])
+    print("  chunk4 A: loop-top/after-tma/pre-arrive/post-arrive:", [rel(k) for k in range(27, 31)])
