@@ -65,6 +65,7 @@ constexpr int kEpiThreads = 128;
 constexpr int kEpiRegs = ED_EPI_REGS;
 constexpr int kProdRegs = ED_PROD_REGS;
 static_assert(kEpiThreads * kEpiRegs + (kThreadsTC - kEpiThreads) * kProdRegs <= 65536, "register budget");
+static_assert(kStages <= ED_LOADER_WARPS, "one owning loader warp per ring stage");
 
 
 // ------------------------------------------------------------------------------------------------
@@ -122,6 +123,22 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t *bar, uint32_t parity) {
 #else
   mbar_wait(bar, parity);
 #endif
+}
+// Wait with a back-off between probes (for waiters off the K-loop's critical path: fewer probes
+// competing with the ring's barrier traffic).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t addr = smem_u32(bar), ok = 0, spins = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) break;
+    if (++spins > (1u << 28)) __trap();
+    __nanosleep(ns);
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -349,6 +366,12 @@ __device__ __forceinline__ int ld_acquire_s32(const int *a) {
 #endif
 #ifndef ED_TMA_ONE_ARRIVE
 #define ED_TMA_ONE_ARRIVE 0  // measured neutral
+#endif
+#ifndef ED_TMA_ROTATE
+#define ED_TMA_ROTATE 1  // TMA box of a stage issued by loader warp (stage mod 6): cfg3 149.5 -> 146.4 us
+#endif
+#ifndef ED_EPI_WAIT_SLEEP
+#define ED_EPI_WAIT_SLEEP 0
 #endif
 #ifndef ED_POLL_NS
 #define ED_POLL_NS 32  // back-off between readiness polls
@@ -1097,7 +1120,11 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
   }
 #pragma unroll
   for (int q = 0; q < NH; ++q) ldcg_v8(q == 0 ? hp0 : hp1, hbuf[0][q], hbuf[1][q]);  // both halves of pair 0
+#if ED_EPI_WAIT_SLEEP > 0
+  mbar_wait_sleep(tfull_bar, parity, ED_EPI_WAIT_SLEEP);
+#else
   mbar_wait_warp(tfull_bar, parity);
+#endif
   tc_fence_after();
   if (tr != nullptr && r == 0) *tr = globaltimer();
   __nv_bfloat16 *H = static_cast<__nv_bfloat16 *>(p.H);
@@ -1673,7 +1700,9 @@ if (warp == 4) {
           const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
           mbar_wait_warp(full + stg, (pipe.it / kStages) & 1u);
+#ifndef ED_EXP_NOFENCE
           fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
+#endif
           tc_fence_after();
           ED_TRACE(p, s, 3, lane == 0 && kc0 == 0 && t == 0);
 #ifdef ED_CHUNK_TRACE  // development: when each stage of item 0 became full (MMA side)
@@ -1832,7 +1861,36 @@ if (warp == 4) {
           }
           const uint32_t stg = pipe.it % kStages;
           bool tma_stage = false;
+#if ED_TMA_ROTATE >= 2
+          // Stage ownership: loader warp (stage index) alone waits on a stage's empty barrier (so no
+          // warp ever waits on a phase two uses ahead).  A stage read by one TMA box is handled by
+          // its owner alone (one arrival of count 192 for the loader threads); a gathered stage is
+          // released to all loader warps by a named barrier after the owner's wait.
+          {
+            const int sgq = (kc0 * kChunkK >= h) ? 1 : 0;
+            const int cbq = (nk == 1 && kps == 1) ? (sgq ? cb[1] : cb[0]) : -1;
+            const bool own = (lt >> 5) == static_cast<int>(stg);
+            if (cbq >= 0) {
+              if (own) {
+                mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+                uint8_t *a_dst = stages + stg * kStageBytes;
+                const int col0q = kc0 * kChunkK - sgq * h;
+                mbar_arrive_tx_elect(full + stg, kAStage);
+                if (st.cell == kCellMvP)  // U rows: [B a | A b], 2h columns
+                  tma_row_box_elect(a_dst, &p.tm_u, sgq * h + col0q, cbq + row_tile * kTileM, full + stg);
+                else
+                  tma_row_box_elect(a_dst, &p.tm_h128, col0q, cbq + row_tile * kTileM, full + stg);
+                if ((lt & 31) == 0) mbar_arrive_cnt(full + stg, kLoaderThreads);
+              }
+              ++pipe.it;
+              continue;
+            }
+            if (own) mbar_wait(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+            asm volatile("bar.sync 3, %0;" ::"n"(kLoaderThreads) : "memory");
+          }
+#else
           mbar_wait_warp(empty + stg, ((pipe.it / kStages) & 1u) ^ 1u);
+#endif
 #ifdef ED_CHUNK_TRACE  // development: when the operand loaders got each stage of item 0
           ED_TRACE(p, s, 48 + min(15, (kc0 - kbeg) / kps), lt == 0 && t == 0);
 #endif
@@ -1857,7 +1915,13 @@ if (warp == 4) {
           const int cbase = kps == 1 ? (seg == 0 ? cb[0] : cb[1]) : -1;
           tma_stage = cbase >= 0;
           if (cbase >= 0) {
+            // the stage's TMA box is issued by loader warp (stage mod #loader warps): consecutive
+            // chunks' issues run on different warps instead of one after another on warp 6
+#if ED_TMA_ROTATE
+            if ((lt >> 5) == static_cast<int>(stg % ED_LOADER_WARPS)) {
+#else
             if (lt < 32) {  // warp-converged; one elected lane issues
+#endif
               mbar_arrive_tx_elect(full + stg, kAStage);
               if (st.cell == kCellMvP)  // U rows: [B a | A b], 2h columns
                 tma_row_box_elect(a_dst, &p.tm_u, seg * h + col0, cbase + row_tile * kTileM, full + stg);
