@@ -325,3 +325,27 @@ def test_comparator_policies_bit_exact_with_oracle(policy):
         plan = E.ed_plan(wl.graphs, wl.types, [], policy=pol)
         m = Merged(wl.graphs, len(wl.types))
         assert [(t, sorted(b)) for t, b in plan.schedule()] == ref(m), wl.name
+
+
+def test_split_k_pairs_planned_for_small_tree_batches(monkeypatch):
+    """Split-K over CTA pairs (reading A-28): the bf16 planner splits exactly the
+    TreeLSTM / TreeGRU internal batches whose 16-unit tiles fill at most half a wave
+    (2 x ceil(m / 128) x h / 16 <= 148), never the leaf or output batches, never the fp32 path,
+    and not at all with ED_SPLIT=0."""
+    from paper_2302_03851_b200 import edbatch as EB
+    for name in ("cfg3", "cfg3_gru"):
+        wl = W.config(name)
+        learned = EB.ed_fsm_learn(wl.graphs, wl.types, merged=True)
+        plan = EB.ed_plan(wl.graphs, wl.types, learned.table, layout=EB.ED_LAYOUT_SCHEDULE_ORDER)
+        sched = plan.schedule()
+        internal = [len(mem) for t, mem in sched if wl.types[t].name.startswith("I")]
+        h = wl.hidden
+        expect = sum(1 for m in internal if 2 * ((m + 127) // 128) * (h // 16) <= 148)
+        assert expect >= 5
+        assert plan.info["split_steps"] == expect, (name, internal)
+    wl = W.config("cfg1")  # fp32: no tensor-core tiles, no split
+    assert _plan(wl).info["split_steps"] == 0
+    monkeypatch.setenv("ED_SPLIT", "0")
+    wl = W.config("cfg3")
+    learned = E.ed_fsm_learn(wl.graphs, wl.types, merged=True)
+    assert E.ed_plan(wl.graphs, wl.types, learned.table).info["split_steps"] == 0
