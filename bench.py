@@ -456,6 +456,10 @@ def main():
     workers = max(1, min(args.plan_threads, (os.cpu_count() or 1) - 2))
     pipe = E.PlanPipeline(wl.types, fsm, workers, layout=layout, staging=staging, step_order=step_order)
     h2d = d2h = 0
+    # two workspaces used in turn: the next minibatch's plan is uploaded (H2D + zeroing, on a side
+    # stream) into one while the kernel of the current minibatch runs on the other
+    wss = [ws, E.Workspace(plan)]
+    up_stream = torch.cuda.Stream()
 
     def e2e_run(nsteps):
         nonlocal h2d, d2h
@@ -463,8 +467,9 @@ def main():
         live = []
         for k in range(nsteps):
             p2 = futs[k].result()                                  # host Alg. 1 + layout + lowering
-            ws.plan_info = p2.info
-            E.ed_execute(p2, weights, ws, out)                     # uploads the step table (H2D)
+            w_k = wss[k % 2]
+            w_k.plan_info = p2.info
+            E.ed_execute(p2, weights, w_k, out, upload_stream=up_stream)  # step table H2D on the side stream
             res = rg() if rg else out
             host_out[k % 2].copy_(res, non_blocking=True)          # D2H of the step's result
             h2d, d2h = p2.upload_bytes, host_out[0].numel() * host_out[0].element_size()
@@ -485,6 +490,8 @@ def main():
     pipe.close()
     e2e_times = [a.elapsed_time(b) / args.e2e_steps]
     ws.plan_info = plan.info
+    for w_ in wss[1:]:
+        w_.release()
     e2e_ms = statistics.median(e2e_times)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
@@ -557,7 +564,7 @@ def main():
             "e2e": {"value": n_inst_total / (e2e_ms / 1e3), "unit": "instances/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "includes": "per step: ed_plan (host Alg. 1 + layout + lowering, on a pool of host threads "
-                                "overlapping the GPU) + step-table/token H2D + ed_execute + root D2H",
+                                "overlapping the GPU) + step-table/token H2D (side stream, two workspaces in turn) + ed_execute + root D2H",
                     "plan_threads": workers},
             "gpu_launches": args.steps * plan.launches,
             "clocks": clock_rec,

@@ -228,6 +228,11 @@ typedef struct {
                        instance order (may be NULL) */
   uint64_t *trace;  /* optional device buffer [num_steps x 64] of %globaltimer stamps taken by
                        CTA 0 at fixed phases of each batch (profiling aid; NULL = off) */
+  void *upload_stream;  /* optional cudaStream_t for the binding work of an execute that binds (the
+                       static part's H2D and the zeroing): it is ordered after the previous launch
+                       on this workspace, and the launch stream waits for it.  With two workspaces
+                       used in turn, the next minibatch's upload overlaps the running kernel.
+                       NULL: everything on the launch stream. */
 } ed_io_t;
 
 /* Build a plan (host only; no CUDA call).  Validates the graphs (errors above), merges them

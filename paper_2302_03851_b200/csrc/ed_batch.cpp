@@ -126,6 +126,11 @@ struct WsBinding {
 struct WsRegistry {
   std::mutex mu;
   std::map<const void *, WsBinding> owner;  // workspace -> binding
+  // workspace -> event recorded on the launch stream after its last launch (kept for the process:
+  // an upload on a side stream waits for it before overwriting the workspace's static part)
+  std::map<const void *, cudaEvent_t> done;
+  cudaEvent_t up_ev[16] = {};  // ring of events ordering side-stream uploads before their launches
+  int up_next = 0;
   uint64_t next_nonce = 0x5EDB000000000001ull;
 };
 WsRegistry &ws_registry() {
@@ -1174,6 +1179,9 @@ ed_status_t ed_workspace_release(const void *ws) {
 
 ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, void *ws, size_t ws_bytes,
                        void *stream) {
+  static const bool prof = std::getenv("ED_EXEC_TIMING") != nullptr;  // development: host phase times
+  double tp[8] = {};
+  if (prof) tp[0] = now_us();
   if (!pl || !w) return fail(ED_E_INVALID_ARG, "null argument");
   if (!ws || (reinterpret_cast<uintptr_t>(ws) & 1023) != 0) return fail(ED_E_WORKSPACE, "workspace null or not 1024-aligned");
   if (ws_bytes < pl->ws_bytes) return fail(ED_E_WORKSPACE, "workspace too small: need " + std::to_string(pl->ws_bytes));
@@ -1210,6 +1218,7 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
   if (major != 10 || minor != 0) return fail(ED_E_UNSUPPORTED, "device is not sm_100 (sm_" + std::to_string(major * 10 + minor) + ")");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t *base = static_cast<uint8_t *>(ws);
+  if (prof) tp[1] = now_us();
   bool need_upload;
   uint64_t nonce = 0;
   uint32_t seq = 0;
@@ -1225,22 +1234,40 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
       nonce = reg.next_nonce++;
     }
   }
+  // the binding work runs on io->upload_stream when given (after this workspace's last launch),
+  // and the launch stream waits for it
+  cudaStream_t su = (io && io->upload_stream) ? static_cast<cudaStream_t>(io->upload_stream) : s;
+  cudaEvent_t ws_done = nullptr, up_ev = nullptr;
+  if (need_upload && su != s) {
+    WsRegistry &reg = ws_registry();
+    std::lock_guard<std::mutex> lk(reg.mu);
+    auto it = reg.done.find(ws);
+    if (it != reg.done.end()) ws_done = it->second;
+    cudaEvent_t &ev = reg.up_ev[reg.up_next];
+    reg.up_next = (reg.up_next + 1) % 16;
+    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+      return fail(ED_E_CUDA, "cudaEventCreate failed");
+    up_ev = ev;
+  }
   if (need_upload) {
     // bind: upload the static part with the binding nonce in its header, zero the readiness counters
     std::memcpy(pl->blob.data(), &nonce, sizeof(nonce));
-    cudaError_t ce = upload_async(base + pl->off_bar, pl->blob.data(), pl->blob.size(), s);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_ready, 0, 4 * static_cast<size_t>(pl->V + 1), s);
+    if (ws_done && cudaStreamWaitEvent(su, ws_done, 0) != cudaSuccess)
+      return fail(ED_E_CUDA, "cudaStreamWaitEvent failed");
+    cudaError_t ce = upload_async(base + pl->off_bar, pl->blob.data(), pl->blob.size(), su);
+    if (prof) tp[2] = now_us();
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_ready, 0, 4 * static_cast<size_t>(pl->V + 1), su);
     if (ce == cudaSuccess) {
       const size_t elt = pl->dtype == ED_BF16 ? 2 : 4;
       // zero row V and the staged rows (zero-state entries are never written by a producer)
-      ce = cudaMemsetAsync(base + pl->off_h + elt * pl->V * pl->hidden, 0, elt * pl->hidden * (1 + pl->op_rows), s);
-      if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_c + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
+      ce = cudaMemsetAsync(base + pl->off_h + elt * pl->V * pl->hidden, 0, elt * pl->hidden * (1 + pl->op_rows), su);
+      if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_c + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), su);
       if (ce == cudaSuccess && pl->need_x)
-        ce = cudaMemsetAsync(base + pl->off_x + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), s);
+        ce = cudaMemsetAsync(base + pl->off_x + 4 * pl->V * pl->hidden, 0, 4 * static_cast<size_t>(pl->hidden), su);
       if (ce == cudaSuccess && pl->need_mv) {
         const size_t hh = static_cast<size_t>(pl->hidden);
-        ce = cudaMemsetAsync(base + pl->off_u + elt * pl->V * 2 * hh, 0, elt * 2 * hh, s);
-        if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_m + elt * pl->V * hh * hh, 0, elt * hh * hh, s);
+        ce = cudaMemsetAsync(base + pl->off_u + elt * pl->V * 2 * hh, 0, elt * 2 * hh, su);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(base + pl->off_m + elt * pl->V * hh * hh, 0, elt * hh * hh, su);
       }
     }
     if (ce != cudaSuccess) return fail(ED_E_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
@@ -1251,6 +1278,7 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
     b.nonce = nonce;
     b.seq = seq = 1;
   }
+  if (prof) tp[3] = now_us();
   if (pl->grid == 0) {
     e = ed::persistent_grid(pl->dtype, pl->has_split, &pl->grid);
     if (e) return fail(ED_E_CUDA, std::string("occupancy: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -1304,7 +1332,25 @@ ed_status_t ed_execute(ed_plan_t *pl, const ed_weights_t *w, const ed_io_t *io, 
     }
   }
   p.has_split = pl->has_split ? 1 : 0;
+  if (up_ev) {  // the launch waits for the side-stream binding work
+    if (cudaEventRecord(up_ev, su) != cudaSuccess || cudaStreamWaitEvent(s, up_ev, 0) != cudaSuccess)
+      return fail(ED_E_CUDA, "ordering the upload stream before the launch failed");
+  }
+  if (prof) tp[4] = now_us();
   e = ed::launch_persistent(p, pl->dtype, pl->grid, pl->has_split, stream);
+  if (e == 0 && io && io->upload_stream) {  // for the next side-stream upload into this workspace
+    WsRegistry &reg = ws_registry();
+    std::lock_guard<std::mutex> lk(reg.mu);
+    cudaEvent_t &ev = reg.done[ws];
+    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) ev = nullptr;
+    if (ev) cudaEventRecord(ev, s);
+  }
+  if (prof) {
+    tp[5] = now_us();
+    std::fprintf(stderr, "ed_execute us: checks %.1f bind+upload %.1f memsets %.1f params %.1f launch %.1f (blob %zu B)\n",
+                 tp[1] - tp[0], tp[2] > 0 ? tp[2] - tp[1] : 0.0, tp[2] > 0 ? tp[3] - tp[2] : 0.0, tp[4] - tp[3],
+                 tp[5] - tp[4], pl->blob.size());
+  }
   if (e) return fail(ED_E_CUDA, std::string("launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
   return ED_OK;
 }

@@ -23,6 +23,7 @@
 #include <stdint.h>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <cstdlib>
 
 #include "ed_internal.h"
@@ -2103,10 +2104,37 @@ int launch_pack(int cell, int hidden, int out_dim, int dtype, int which, const f
 // ------------------------------------------------------------------------------------------------
 // launch
 // ------------------------------------------------------------------------------------------------
+static int device_query(int dev, int *sm_count, int *major, int *minor);
 int device_check(int *sm_count, int *major, int *minor) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return static_cast<int>(e);
+  // device attributes do not change: queried once per device
+  constexpr int kMaxDev = 64;
+  static std::mutex mu;
+  static int known[kMaxDev][4] = {};
+  if (dev >= 0 && dev < kMaxDev) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (known[dev][0]) {
+      *sm_count = known[dev][1];
+      *major = known[dev][2];
+      *minor = known[dev][3];
+      return 0;
+    }
+  }
+  const int r = device_query(dev, sm_count, major, minor);
+  if (r == 0 && dev >= 0 && dev < kMaxDev) {
+    std::lock_guard<std::mutex> lk(mu);
+    known[dev][1] = *sm_count;
+    known[dev][2] = *major;
+    known[dev][3] = *minor;
+    known[dev][0] = 1;
+  }
+  return r;
+}
+
+static int device_query(int dev, int *sm_count, int *major, int *minor) {
+  cudaError_t e;
   e = cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev);
@@ -2133,7 +2161,33 @@ static void cluster2_config(cudaLaunchConfig_t *cfg, cudaLaunchAttribute *at, in
   cfg->numAttrs = cooperative ? 2 : 1;
 }
 
+static int persistent_grid_uncached(int dtype, bool cluster2, int *grid);
+// The occupancy queries cost tens of us per call: one result per (device, dtype, cluster launch),
+// so a serving loop's new minibatch plans do not pay them on every first execute.
 int persistent_grid(int dtype, bool cluster2, int *grid) {
+  constexpr int kMaxDev = 64;
+  static std::mutex mu;
+  static int cache[kMaxDev][2][2] = {};
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return static_cast<int>(ce);
+  const int d = dtype == ED_BF16 ? 1 : 0, c = cluster2 ? 1 : 0;
+  if (dev >= 0 && dev < kMaxDev) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache[dev][d][c] > 0) {
+      *grid = cache[dev][d][c];
+      return 0;
+    }
+  }
+  const int e = persistent_grid_uncached(dtype, cluster2, grid);
+  if (e == 0 && dev >= 0 && dev < kMaxDev) {
+    std::lock_guard<std::mutex> lk(mu);
+    cache[dev][d][c] = *grid;
+  }
+  return e;
+}
+
+static int persistent_grid_uncached(int dtype, bool cluster2, int *grid) {
   int sms = 0, major = 0, minor = 0;
   int e = device_check(&sms, &major, &minor);
   if (e) return e;

@@ -85,7 +85,7 @@ class ed_weights_t(ctypes.Structure):
 
 
 class ed_io_t(ctypes.Structure):
-    _fields_ = [("out_root", ctypes.c_void_p), ("trace", ctypes.c_void_p)]
+    _fields_ = [("out_root", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("upload_stream", ctypes.c_void_p)]
 
 
 class ed_rl_config_t(ctypes.Structure):
@@ -520,7 +520,7 @@ class Workspace:
 
 
 def ed_execute(plan: Plan, weights: DeviceWeights, workspace: Workspace, out_root: Optional[torch.Tensor] = None,
-               stream=None, trace: Optional[torch.Tensor] = None) -> None:
+               stream=None, trace: Optional[torch.Tensor] = None, upload_stream=None) -> None:
     info = plan.info
     if out_root is not None:
         want = torch.bfloat16 if info["dtype"] == ED_BF16 else torch.float32
@@ -532,7 +532,8 @@ def ed_execute(plan: Plan, weights: DeviceWeights, workspace: Workspace, out_roo
                                   and trace.numel() >= info["num_steps"] * 64 + 148 * 4):
         raise ValueError("trace must be a contiguous CUDA int64 tensor of >= num_steps * 64 + 148 * 4 elements")
     io = ed_io_t(ctypes.c_void_p(out_root.data_ptr()) if out_root is not None else None,
-                 ctypes.c_void_p(trace.data_ptr()) if trace is not None else None)
+                 ctypes.c_void_p(trace.data_ptr()) if trace is not None else None,
+                 ctypes.c_void_p(upload_stream.cuda_stream) if upload_stream is not None else None)
     _check(LIB.ed_execute(plan.handle, ctypes.byref(weights.struct), ctypes.byref(io),
                           ctypes.c_void_p(workspace.ptr), workspace.nbytes, _stream_handle(stream)))
 
