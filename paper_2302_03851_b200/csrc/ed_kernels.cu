@@ -1149,11 +1149,7 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
     mbar_wait_cluster(x.xfull, x.par);
   }
 #pragma unroll 1
-#ifdef ED_EXP_NOEPI  // experiment (wrong results): the leaf's epilogue does no pass
-  for (int sp0 = 0; sp0 < (warp_live && CELL != ED_CELL_TREELSTM_LEAF ? nsteps : 0); sp0 += 2) {
-#else
   for (int sp0 = 0; sp0 < (warp_live ? nsteps : 0); sp0 += 2) {
-#endif
   uint4 hlo = make_uint4(0, 0, 0, 0);  // bf16 h of the pair's first half, stored with the second
 #pragma unroll
   for (int b2 = 0; b2 < 2; ++b2) {
@@ -1701,9 +1697,7 @@ if (warp == 4) {
           const int nk = min(kps, kend - kc0);
           const uint32_t stg = pipe.it % kStages;
           mbar_wait_warp(full + stg, (pipe.it / kStages) & 1u);
-#ifndef ED_EXP_NOFENCE
           fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tcgen05.mma (async proxy)
-#endif
           tc_fence_after();
           ED_TRACE(p, s, 3, lane == 0 && kc0 == 0 && t == 0);
 #ifdef ED_CHUNK_TRACE  // development: when each stage of item 0 became full (MMA side)
@@ -1738,16 +1732,11 @@ if (warp == 4) {
 #ifdef ED_CHUNK_TRACE  // development: when the weight loader got each stage of item 0
           ED_TRACE(p, s, 11 + min(15, (kc0 - kbeg) / kps), lane == 0 && t == 0);
 #endif
-#ifdef ED_EXP_HALFB  // experiment (wrong results): the first step loads half of each B chunk
-          const uint32_t nbx = (s >= 1 && s <= 6) ? nb / 2 : nb;
-#else
-          const uint32_t nbx = nb;
-#endif
-          mbar_arrive_tx_elect(full + stg, nbx * nk);
+          mbar_arrive_tx_elect(full + stg, nb * nk);
           for (int q = 0; q < nk; ++q) {
             const uint8_t *src =
                 Wp + ((static_cast<size_t>(kc0 + q) * ntot + static_cast<size_t>(col_tile) * ncols) * 128);
-            bulk_g2s_elect(stages + stg * kStageBytes + boff + q * bchunk, src, nbx, full + stg);
+            bulk_g2s_elect(stages + stg * kStageBytes + boff + q * bchunk, src, nb, full + stg);
           }
           ++pipe.it;
         }
@@ -1935,12 +1924,7 @@ if (warp == 4) {
           } else {
             if (lt == 0) mbar_arrive(full + stg);  // the TMA arrival slot is unused for this stage
             const uint32_t a_base = smem_u32(a_dst);
-#ifdef ED_EXP_HALFA  // experiment (wrong results): the first step gathers half of each A chunk
-            const int nrows_x = (s >= 1 && s <= 6) ? nrows / 2 : nrows;
-#else
-            const int nrows_x = nrows;
-#endif
-            for (int c = lt; c < nrows_x * 8; c += kLoaderThreads) {  // rows past m are not loaded
+            for (int c = lt; c < nrows * 8; c += kLoaderThreads) {  // rows past m are not loaded
               const int r = c >> 3, ch = c & 7;
               const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(lds_ptr(tab + r * 2 + seg)) + col0 + ch * 8;
               cp_async16(a_base + r * 128 + ((ch ^ (r & 7)) << 4), src);
