@@ -183,11 +183,19 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Starts nvidia-smi and returns once it has printed its first sample, so the sampler is
+        live for the whole timed region (a short region otherwise ends before nvidia-smi starts)."""
+        self.first = ""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+        import select
+        r, _, _ = select.select([self.proc.stdout], [], [], 5.0)
+        if r:
+            self.first = self.proc.stdout.readline()
 
     def stop(self, ngpu: int):
         if self.proc is None:
@@ -201,7 +209,7 @@ class ClockSampler:
             out, _ = self.proc.communicate()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in (self.first + (out or "")).strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= ngpu:
                 continue

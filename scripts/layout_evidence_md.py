@@ -17,7 +17,9 @@ for c in ("cfg3", "cfg2", "cfg5"):
             continue
         m = {}
         try:
-            rows = [r for r in csv.reader(open(f"gpurun_out/lay_ncu_{c}_{l}.csv")) if len(r) > 10]
+            rows = list(csv.reader(open(f"gpurun_out/lay_ncu_{c}_{l}.csv")))
+            start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+            rows = [r for r in rows[start:] if len(r) > 10]
             hdr = rows[0]
             for r in rows[1:]:
                 m[r[hdr.index("Metric Name")]] = (float(r[hdr.index("Metric Value")].replace(",", "")),
