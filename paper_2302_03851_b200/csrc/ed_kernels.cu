@@ -2148,7 +2148,21 @@ static void cluster2_config(cudaLaunchConfig_t *cfg, cudaLaunchAttribute *at, in
 static int persistent_grid_uncached(int dtype, bool cluster2, int *grid);
 // The occupancy queries cost tens of us per call: one result per (device, dtype, cluster launch),
 // so a serving loop's new minibatch plans do not pay them on every first execute.
+static int persistent_grid_cached(int dtype, bool cluster2, int *grid);
+// ED_GRID_MAX (testing): cap the persistent grid (rounded down to even for cluster launches), so
+// that batches get several tiles per CTA (split-K pairs exchange more than once per batch).
 int persistent_grid(int dtype, bool cluster2, int *grid) {
+  const int e = persistent_grid_cached(dtype, cluster2, grid);
+  const char *cap = std::getenv("ED_GRID_MAX");
+  if (e == 0 && cap && std::atoi(cap) > 0 && *grid > std::atoi(cap)) {
+    *grid = std::atoi(cap);
+    if (cluster2) *grid &= ~1;
+    if (*grid < 2) *grid = 2;
+  }
+  return e;
+}
+
+static int persistent_grid_cached(int dtype, bool cluster2, int *grid) {
   constexpr int kMaxDev = 64;
   static std::mutex mu;
   static int cache[kMaxDev][2][2] = {};

@@ -275,3 +275,17 @@ def test_minibatch_of_only_external_roots_and_one_op():
     _check(wl)
     wl.graphs = words
     _check(wl)
+
+
+@pytest.mark.parametrize("grid_max", ["64", "22"])
+def test_split_k_pairs_with_several_tiles_per_cta(grid_max, monkeypatch):
+    """Split-K pairs (A-28) when a batch has more tile pairs than CTA pairs: with the
+    persistent grid capped (ED_GRID_MAX) every CTA exchanges partial sums for several tiles of one
+    batch in turn (the xfree / xfull phases alternate within the batch).  TreeLSTM and TreeGRU
+    forests at h = 512, where the small batches are split."""
+    monkeypatch.setenv("ED_GRID_MAX", grid_max)
+    for cell in ("treelstm", "treegru"):
+        wl = W.treelstm(24, (2, 30), 512, "bf16", cfg=95, cell=cell)
+        plan, _, _, _, _ = _check(wl)
+        assert plan.info["split_steps"] > 0
+        assert plan.query_info()["grid"] == int(grid_max)
