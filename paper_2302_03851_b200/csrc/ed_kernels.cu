@@ -1139,14 +1139,26 @@ __device__ __forceinline__ void umma_epilogue(const KParams &p, const DevStep &s
 #pragma unroll
     for (int g = 0; g < G; ++g) tmem_ld8(tacc + static_cast<uint32_t>(g * 16 + (x.rank ^ 1) * 8), zs[g]);
     tmem_wait_ld();
+#ifdef ED_SPLIT_TRACE
+    if (tr != nullptr && r == 0) tr[8] = globaltimer();
+#endif
     mbar_wait_cluster(x.xfree, x.par);
+#ifdef ED_SPLIT_TRACE
+    if (tr != nullptr && r == 0) tr[9] = globaltimer();
+#endif
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
       for (int q = 0; q < 2; ++q)
         st_async_v4(x.rrecv + static_cast<uint32_t>(((2 * g + q) * kTileM + r) * 16), zs[g][4 * q], zs[g][4 * q + 1],
                     zs[g][4 * q + 2], zs[g][4 * q + 3], x.rxfull);
+#ifdef ED_SPLIT_TRACE
+    if (tr != nullptr && r == 0) tr[10] = globaltimer();
+#endif
     mbar_wait_cluster(x.xfull, x.par);
+#ifdef ED_SPLIT_TRACE
+    if (tr != nullptr && r == 0) tr[11] = globaltimer();
+#endif
   }
 #pragma unroll 1
   for (int sp0 = 0; sp0 < (warp_live ? nsteps : 0); sp0 += 2) {

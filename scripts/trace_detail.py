@@ -32,3 +32,5 @@ for s in range(nb):
     print("  B stage free:", [rel(k) for k in range(11, 27) if t[s, k]])
     print("  stage full:  ", [rel(k) for k in range(32, 48) if t[s, k]])
     print("  chunk4 A: loop-top/after-tma/pre-arrive/post-arrive:", [rel(k) for k in range(27, 31)])
+    if t[s, 14]:
+        print("  split exchange: partner-ld/xfree/sent/xfull:", [rel(k) for k in (14, 15, 16, 17)])
