@@ -289,3 +289,28 @@ def test_split_k_pairs_with_several_tiles_per_cta(grid_max, monkeypatch):
         plan, _, _, _, _ = _check(wl)
         assert plan.info["split_steps"] > 0
         assert plan.query_info()["grid"] == int(grid_max)
+
+
+def test_side_stream_uploads_into_two_workspaces_match_serial():
+    """ed_io_t.upload_stream (the serving loop's overlap): a sequence of different minibatch plans
+    executed in turn on two workspaces, each binding upload on a side stream ordered after the
+    workspace's previous launch, gives the bitwise-same instance outputs as executing each plan
+    alone on a fresh workspace with everything on one stream."""
+    from paper_2302_03851_b200 import edbatch as E
+    wls = [W.treelstm(30 + 4 * k, (2, 24), 256, "bf16", cfg=80 + k) for k in range(6)]
+    ref = []
+    for wl in wls:
+        plan, w, ws, out = run_gpu(wl)
+        ref.append(out.clone())
+    ws_w = [E.DeviceWeights(wl.types, wl.params) for wl in wls]
+    plans = [E.ed_plan(wl.graphs, wl.types, E.fsm_from_priority(wl.priority, len(wl.types))) for wl in wls]
+    big = max(plans, key=lambda p: p.info["workspace_bytes"])
+    wss = [E.Workspace(big), E.Workspace(big)]
+    up = torch.cuda.Stream()
+    outs = [torch.zeros_like(r) for r in ref]
+    for rep in range(2):
+        for k, (plan, o) in enumerate(zip(plans, outs)):
+            E.ed_execute(plan, ws_w[k], wss[k % 2], o, upload_stream=up)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, ref):
+        assert torch.equal(o, r)
