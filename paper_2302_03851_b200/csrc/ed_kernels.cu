@@ -67,6 +67,7 @@ constexpr int kEpiRegs = ED_EPI_REGS;
 constexpr int kProdRegs = ED_PROD_REGS;
 static_assert(kEpiThreads * kEpiRegs + (kThreadsTC - kEpiThreads) * kProdRegs <= 65536, "register budget");
 static_assert(kStages <= ED_LOADER_WARPS, "one owning loader warp per ring stage");
+static_assert(kThreadsTC % 128 == 0, "setmaxnreg acts on whole warpgroups: 4 + 2 + loader warps = 4k warps");
 
 
 // ------------------------------------------------------------------------------------------------
