@@ -362,7 +362,8 @@ def main():
     ap.add_argument("--fsm", default="learned", choices=["learned", "learned_instance", "priority"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=8)
-    ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--e2e-steps", type=int, default=300,
+                    help="minibatches of the end-to-end serving loop (planning pipeline fill amortised over them)")
     ap.add_argument("--plan-threads", type=int, default=14, help="host threads planning minibatches ahead (e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -471,10 +472,14 @@ def main():
 
     def e2e_run(nsteps):
         nonlocal h2d, d2h
-        futs = [pipe.submit(batch) for _ in range(nsteps)]
+        window = 2 * workers                                       # minibatches planned ahead (bounded memory)
+        futs = [pipe.submit(batch) for _ in range(min(nsteps, window))]
         live = []
         for k in range(nsteps):
             p2 = futs[k].result()                                  # host Alg. 1 + layout + lowering
+            futs[k] = None
+            if k + window < nsteps:
+                futs.append(pipe.submit(batch))
             w_k = wss[k % 2]
             w_k.plan_info = p2.info
             E.ed_execute(p2, weights, w_k, out, upload_stream=up_stream)  # step table H2D on the side stream
