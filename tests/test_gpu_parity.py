@@ -314,3 +314,18 @@ def test_side_stream_uploads_into_two_workspaces_match_serial():
     torch.cuda.synchronize()
     for o, r in zip(outs, ref):
         assert torch.equal(o, r)
+
+
+def test_split_disabled_and_enabled_both_match_the_oracle(monkeypatch):
+    """The split-K pairs change only the fp32 summation order (A-28): with ED_SPLIT=0 (no clusters,
+    one CTA per tile) and with the default both paths meet the parity tolerance, and they differ
+    from each other by less than it."""
+    wl = W.treelstm(16, (2, 30), 512, "bf16", cfg=96)
+    monkeypatch.setenv("ED_SPLIT", "0")
+    plan0, _, _, out0, _ = _check(wl)
+    assert plan0.info["split_steps"] == 0
+    monkeypatch.setenv("ED_SPLIT", "1")
+    plan1, _, _, out1, _ = _check(wl)
+    assert plan1.info["split_steps"] > 0
+    d = (out0.float() - out1.float()).abs().max().item()
+    assert d <= TOL[wl.dtype]
