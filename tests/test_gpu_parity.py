@@ -329,3 +329,19 @@ def test_split_disabled_and_enabled_both_match_the_oracle(monkeypatch):
     assert plan1.info["split_steps"] > 0
     d = (out0.float() - out1.float()).abs().max().item()
     assert d <= TOL[wl.dtype]
+
+
+def test_split_k_plan_with_simt_tagger_steps():
+    """One plan mixing TreeLSTM trees (whose small internal batches run split-K over CTA pairs, so
+    the kernel is a cluster launch) with BiLSTM-tagger chains (whose tagger output runs as SIMT
+    steps reusing the shared memory the split-K exchange also uses): both families meet the oracle."""
+    import dataclasses
+    tl = W.treelstm(12, (2, 24), 256, "bf16", cfg=97)
+    bl = W.bilstm(10, (4, 20), 256, "bf16", cfg=98)
+    nt, nw = len(tl.types), len(tl.params)
+    types = list(tl.types) + [dataclasses.replace(t, weight_set=t.weight_set + nw) for t in bl.types]
+    graphs = list(tl.graphs) + [W.Graph(g.type + nt, g.in_off, g.in_idx, g.ext, g.root) for g in bl.graphs]
+    prio = list(tl.priority) + [p + nt for p in bl.priority]
+    wl = W.Workload("mixed", types, graphs, prio, list(tl.params) + list(bl.params), "bf16", 256)
+    plan, _, _, _, _ = _check(wl)
+    assert plan.info["split_steps"] > 0
